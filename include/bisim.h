@@ -1,0 +1,148 @@
+/*
+ * bisim.h -- C ABI of libbisim.so, the B200 (sm_100a) implementation of the
+ * CRCW-PRAM partition-refinement path of arXiv 2105.11788.
+ *
+ * Drop-in boundary.  The reference `parbisim` exposes this path as two
+ * Python functions:
+ *
+ *   bcrp_run(lts, policy, *, common_election, observer, max_supersteps)
+ *       /root/reference/pkg/src/parbisim/bcrp.py:192-195
+ *   rcpp_run(rel, policy, *, common_election, observer, max_supersteps)
+ *       /root/reference/pkg/src/parbisim/rcpp.py:220-223
+ *
+ * both returning (Partition, RunStats) (lts.py:76-114, lts.py:164-184).  The
+ * functions below replace the bodies of those two calls: transition arrays
+ * in, per-state leader block ids plus the RunStats fields out.  Arrays are
+ * plain C-contiguous int32; no torch or CUDA types appear in the signatures.
+ *
+ * Semantics (bit-exact with the reference under the Priority write policy,
+ * pram.py:153-154, which Common-with-election reproduces identically):
+ *   - block_out[s] is the leader (minimum state, for canonical inputs) of
+ *     s's block; BCRP output is canonical, RCPP keeps pi0's leaders.
+ *   - st->supersteps counts main-loop rounds that selected a splitter;
+ *     splits_out[k] is the number of blocks split in round k+1.
+ *   - The superstep guard counts like PramEngine.begin_superstep
+ *     (pram.py:195-200): BCRP completes iff |Act| + R + 1 <= max_supersteps
+ *     (default 3n + |Act| + 8, bcrp.py:206-207); RCPP iff R + 1 <=
+ *     max_supersteps (default 3n + 9, rcpp.py:234-235).
+ *
+ * Return codes map to the reference's exceptions: BISIM_BAD_INPUT ->
+ * ValueError (lts.py:40-52, rcpp.py:49-55), BISIM_GUARD ->
+ * SuperstepLimitError (pram.py:70-71), BISIM_CUDA -> RuntimeError,
+ * BISIM_ABORTED -> the observer's own exception.  bisim_last_error()
+ * returns a thread-local message for the last failing call.
+ *
+ * There is no CPU fallback: without a CUDA device every compute entry point
+ * returns BISIM_CUDA.
+ */
+#ifndef BISIM_H
+#define BISIM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BISIM_OK 0
+#define BISIM_BAD_INPUT 1
+#define BISIM_GUARD 2
+#define BISIM_CUDA 3
+#define BISIM_ABORTED 4
+
+/* max_supersteps value meaning "the reference default" (max_supersteps=None) */
+#define BISIM_DEFAULT_GUARD INT64_MIN
+
+/* Execution strategies of the refinement loop. */
+#define BISIM_MODE_AUTO 0
+#define BISIM_MODE_PERSISTENT 1 /* one cooperative kernel runs every round */
+#define BISIM_MODE_STEPPED 2    /* one launch per round (observer support) */
+
+typedef struct bisim_stats {
+    int64_t supersteps;      /* RunStats.supersteps */
+    int64_t label_rounds;    /* |Act| label pre-partition rounds (BCRP) */
+    int64_t guard_count;     /* superstep counter when BISIM_GUARD fired */
+    int32_t initial_blocks;  /* RunStats.initial_block_count */
+    int32_t final_blocks;    /* RunStats.final_block_count */
+    int64_t mark_length;     /* BcrpAux.mark_length (n for RCPP) */
+    double t_h2d_ms;         /* CUDA-event times on the library stream */
+    double t_pre_ms;
+    double t_label_ms;
+    double t_alg_ms;
+    double t_d2h_ms;
+    int64_t bytes_alg;       /* algorithmic bytes of the main loop */
+    int32_t kernel_launches; /* kernels this call launched */
+    int32_t mode;            /* BISIM_MODE_* actually used */
+} bisim_stats;
+
+/* observer(iteration, block, n, user): called after every counted round in
+ * stepped mode with a host copy of the block array (bcrp.py:307-308).  A
+ * non-zero return aborts the run with BISIM_ABORTED. */
+typedef int (*bisim_observer_fn)(int64_t iteration, const int32_t *block, int32_t n, void *user);
+
+typedef struct bisim_options {
+    int32_t device;          /* CUDA ordinal */
+    int32_t mode;            /* BISIM_MODE_* */
+    bisim_observer_fn observer;
+    void *observer_user;
+} bisim_options;
+
+/* ---- host-pointer entry points (the reference-facing boundary) ---------- */
+
+/* bcrp_run: transitions (src[i], act[i], dst[i]), i < m, act in [0, num_actions). */
+int bisim_bcrp(int32_t n, int64_t m, int32_t num_actions, const int32_t *src, const int32_t *act,
+               const int32_t *dst, int64_t max_supersteps, int32_t *block_out,
+               int32_t *splits_out, int64_t splits_cap, bisim_stats *st, int device);
+
+/* rcpp_run: edges (src[i], dst[i]) and pi0 in leader form (rcpp.py:38-55). */
+int bisim_rcpp(int32_t n, int64_t m, const int32_t *src, const int32_t *dst,
+               const int32_t *pi0_leader, int64_t max_supersteps, int32_t *block_out,
+               int32_t *splits_out, int64_t splits_cap, bisim_stats *st, int device);
+
+/* Same, with options (observer / forced mode). opt may be NULL. */
+int bisim_bcrp_ex(int32_t n, int64_t m, int32_t num_actions, const int32_t *src,
+                  const int32_t *act, const int32_t *dst, int64_t max_supersteps,
+                  int32_t *block_out, int32_t *splits_out, int64_t splits_cap, bisim_stats *st,
+                  const bisim_options *opt);
+int bisim_rcpp_ex(int32_t n, int64_t m, const int32_t *src, const int32_t *dst,
+                  const int32_t *pi0_leader, int64_t max_supersteps, int32_t *block_out,
+                  int32_t *splits_out, int64_t splits_cap, bisim_stats *st,
+                  const bisim_options *opt);
+
+/* ---- device-pointer entry points (inputs already resident in HBM) ------- */
+/* src/act/dst/pi0 and block_out are device pointers on opt->device;
+ * splits_out is a host pointer.  The call is synchronous. */
+int bisim_bcrp_device(int32_t n, int64_t m, int32_t num_actions, const int32_t *d_src,
+                      const int32_t *d_act, const int32_t *d_dst, int64_t max_supersteps,
+                      int32_t *d_block_out, int32_t *splits_out, int64_t splits_cap,
+                      bisim_stats *st, const bisim_options *opt);
+int bisim_rcpp_device(int32_t n, int64_t m, const int32_t *d_src, const int32_t *d_dst,
+                      const int32_t *d_pi0_leader, int64_t max_supersteps, int32_t *d_block_out,
+                      int32_t *splits_out, int64_t splits_cap, bisim_stats *st,
+                      const bisim_options *opt);
+
+/* ---- preprocessing tables (bcrp.py:116-126, BcrpAux) -------------------- */
+/* Per ORIGINAL transition index i: order_out[i] = rank of act[i] among
+ * src[i]'s distinct labels; per state: nr_marks_out[s], off_out[s].  Returns
+ * BISIM_OK and *mark_length.  Host pointers. */
+int bisim_preprocess(int32_t n, int64_t m, int32_t num_actions, const int32_t *src,
+                     const int32_t *act, int32_t *order_out, int32_t *nr_marks_out,
+                     int32_t *off_out, int64_t *mark_length, int device);
+
+/* partition_by_outgoing_labels(lts, Priority) (bcrp.py:129-141). */
+int bisim_label_partition(int32_t n, int64_t m, int32_t num_actions, const int32_t *src,
+                          const int32_t *act, int32_t *block_out, int device);
+
+/* ---- misc ---------------------------------------------------------------- */
+const char *bisim_last_error(void);
+int bisim_device_count(void);
+/* The library's CUDA stream on `device` (a cudaStream_t), so callers can
+ * bracket calls with their own CUDA events.  NULL on error. */
+void *bisim_stream(int device);
+/* Library version string (build id). */
+const char *bisim_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BISIM_H */

@@ -1,0 +1,257 @@
+"""Generate golden fixtures by running the UNMODIFIED reference package.
+
+TEST INFRASTRUCTURE ONLY.  Run in the development container, where the
+reference lives at /root/reference (read-only); the outputs under
+tests/golden/ are committed so the GPU box (which has no /root/reference)
+can check against them.
+
+    python oracle/gen_golden.py cases      # small known-answer instances
+    python oracle/gen_golden.py sweep      # acceptance-sweep instances
+    python oracle/gen_golden.py c1         # config c1 full run (~35 min, 1 core)
+
+Every fixture records the instance (src/act/dst arrays or the generator
+recipe), the reference's Priority-policy outputs (block array in leader form,
+RunStats) and where applicable the per-round observer snapshots.
+"""
+from __future__ import annotations
+
+import gzip
+import json
+import os
+import random
+import sys
+import time
+
+import numpy as np
+
+REF_SRC = "/root/reference/pkg/src"
+REF_TESTS = "/root/reference/pkg/tests"
+OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden")
+
+
+def _ref():
+    if REF_SRC not in sys.path:
+        sys.path.insert(0, REF_SRC)
+    import parbisim  # noqa: F401
+    return parbisim
+
+
+def lts_arrays(lts):
+    tr = lts.transitions
+    return {
+        "n": lts.n,
+        "num_actions": len(lts.action_labels),
+        "src": [t.source for t in tr],
+        "act": [t.action for t in tr],
+        "dst": [t.target for t in tr],
+    }
+
+
+def run_bcrp(pb, lts, snaps=False, max_supersteps=None):
+    chain = []
+    obs = (lambda k, p: chain.append(list(p.block))) if snaps else None
+    try:
+        part, st = pb.bcrp_run(lts, pb.Priority(), observer=obs, max_supersteps=max_supersteps)
+    except pb.SuperstepLimitError:
+        return {"guard": True, "snapshots": chain if snaps else None}
+    out = {"guard": False, "block": list(part.block), "supersteps": st.supersteps,
+           "splits": list(st.splits_per_iteration), "initial_blocks": st.initial_block_count,
+           "final_blocks": st.final_block_count}
+    if snaps:
+        out["snapshots"] = chain
+    return out
+
+
+def run_rcpp(pb, n, edges, pi0_block, snaps=False, max_supersteps=None):
+    chain = []
+    obs = (lambda k, p: chain.append(list(p.block))) if snaps else None
+    rel = pb.RelationInput(n, tuple(edges), pb.Partition(pi0_block))
+    try:
+        part, st = pb.rcpp_run(rel, pb.Priority(), observer=obs, max_supersteps=max_supersteps)
+    except pb.SuperstepLimitError:
+        return {"guard": True, "snapshots": chain if snaps else None}
+    out = {"guard": False, "block": list(part.block), "supersteps": st.supersteps,
+           "splits": list(st.splits_per_iteration), "initial_blocks": st.initial_block_count,
+           "final_blocks": st.final_block_count}
+    if snaps:
+        out["snapshots"] = chain
+    return out
+
+
+def chain_lts(pb, n):
+    return pb.lts_from_labeled_edges(n, [(i, "a", i + 1) for i in range(n - 1)])
+
+
+def cases():
+    pb = _ref()
+    sys.path.insert(0, REF_TESTS)
+    import _support as sup
+    from parbisim.cli import gen_fanout
+    out = {}
+
+    # preprocessing tables: Fig. 2 instance (test_acceptance.py:239-257) and
+    # the no-outgoing-state instance (test_bcrp.py:105-110)
+    for name, lts in [("fig2", sup.mixed_label_lts()),
+                      ("no_outgoing", pb.lts_from_labeled_edges(3, [(0, "a", 1), (2, "b", 0)])),
+                      ("stable_sort", pb.lts_from_labeled_edges(2, [(1, "b", 0), (0, "a", 1),
+                                                                    (0, "a", 0)]))]:
+        aux = pb.preprocess(lts)
+        rec = lts_arrays(lts)
+        index = {t: [] for t in set(lts.transitions)}
+        # the sorted permutation: k-th sorted transition = original index perm[k]
+        used = [False] * lts.m
+        perm = []
+        for t in aux.lts.transitions:
+            for i, u in enumerate(lts.transitions):
+                if not used[i] and u == t:
+                    used[i] = True
+                    perm.append(i)
+                    break
+        del index
+        rec.update(perm=perm, action_switch=list(aux.action_switch), order=list(aux.order),
+                   nr_marks=list(aux.nr_marks), off=list(aux.off), mark_length=aux.mark_length,
+                   label_partition=list(pb.partition_by_outgoing_labels(lts, pb.Priority()).block),
+                   bcrp=run_bcrp(pb, lts, snaps=True))
+        out["pre_" + name] = rec
+
+    # Fig. 1 five-state relation (test_rcpp.py:119-136, FIVE_STATE_FINAL)
+    rel = sup.five_state_input()
+    out["five_state"] = {"n": 5, "src": [e[0] for e in rel.edges], "dst": [e[1] for e in rel.edges],
+                         "pi0": list(rel.pi0.block),
+                         "rcpp": run_rcpp(pb, 5, rel.edges, rel.pi0.block, snaps=True)}
+
+    # Fan_out family (cli.py:62-75): BCRP and RCPP from the trivial partition
+    for n in list(range(3, 65)) + [100, 200]:
+        lts = gen_fanout(n)
+        rec = lts_arrays(lts)
+        rec["bcrp"] = run_bcrp(pb, lts, snaps=(n <= 20))
+        edges = [(t.source, t.target) for t in lts.transitions]
+        rec["rcpp_trivial"] = run_rcpp(pb, n, edges, [0] * n, snaps=(n <= 20))
+        out[f"fanout_{n}"] = rec
+
+    # chains (SURVEY c3 shape): BCRP R = 2n-2, RCPP R = 2n-1
+    for n in (2, 3, 10, 100, 200):
+        lts = chain_lts(pb, n)
+        rec = lts_arrays(lts)
+        rec["bcrp"] = run_bcrp(pb, lts)
+        edges = [(t.source, t.target) for t in lts.transitions]
+        rec["rcpp_trivial"] = run_rcpp(pb, n, edges, [0] * n)
+        out[f"chain_{n}"] = rec
+
+    # edge-free (test_rcpp.py:225-231) and label-only instances
+    lts = pb.lts_from_labeled_edges(4, [], extra_labels=("a", "b"))
+    rec = lts_arrays(lts)
+    rec["bcrp"] = run_bcrp(pb, lts)
+    rec["rcpp_trivial"] = run_rcpp(pb, 4, [], [0] * 4)
+    out["edge_free_4"] = rec
+
+    # guard boundaries: the run completes iff |Act| + R + 1 <= max_supersteps
+    guard = []
+    for n in (4, 8, 12):
+        lts = gen_fanout(n)
+        full = run_bcrp(pb, lts)
+        A = len(lts.action_labels)
+        for g in (0, 1, 2, A, A + full["supersteps"], A + full["supersteps"] + 1):
+            guard.append({"kind": "bcrp", "instance": f"fanout_{n}", "max_supersteps": g,
+                          "result": run_bcrp(pb, lts, max_supersteps=g)})
+        edges = [(t.source, t.target) for t in lts.transitions]
+        rfull = run_rcpp(pb, n, edges, [0] * n)
+        for g in (0, 1, rfull["supersteps"], rfull["supersteps"] + 1):
+            guard.append({"kind": "rcpp_trivial", "instance": f"fanout_{n}", "max_supersteps": g,
+                          "result": run_rcpp(pb, n, edges, [0] * n, max_supersteps=g)})
+    out["guard"] = guard
+
+    # RCPP with non-canonical pi0 leaders (Partition allows any self-led
+    # leader, lts.py:85-95): pi0 is used verbatim (rcpp.py:64)
+    rng = random.Random(7)
+    noncanon = []
+    for idx in range(60):
+        n = rng.randint(1, 30)
+        m = rng.randint(0, 3 * n)
+        edges = [(rng.randrange(n), rng.randrange(n)) for _ in range(m)]
+        k = rng.randint(1, max(1, n // 3))
+        colour = [rng.randrange(k) for _ in range(n)]
+        leader_of = {}
+        for s in range(n):  # leader = LARGEST member of its colour class
+            leader_of[colour[s]] = s
+        pi0 = [leader_of[c] for c in colour]
+        noncanon.append({"n": n, "src": [e[0] for e in edges], "dst": [e[1] for e in edges],
+                         "pi0": pi0, "rcpp": run_rcpp(pb, n, edges, pi0, snaps=True)})
+    out["rcpp_noncanonical"] = noncanon
+
+    # medium random BCRP instances (oracle-finishable, a few seconds each)
+    medium = []
+    for idx, (n, m, A) in enumerate([(300, 1500, 4), (500, 2500, 3), (400, 4000, 8),
+                                     (600, 1800, 1), (250, 2500, 16)]):
+        r = random.Random(1000 + idx)
+        labels = [f"l{j:02d}" for j in range(A)]
+        edges = [(r.randrange(n), labels[r.randrange(A)], r.randrange(n)) for _ in range(m)]
+        lts = pb.lts_from_labeled_edges(n, edges, extra_labels=labels)
+        rec = lts_arrays(lts)
+        rec["bcrp"] = run_bcrp(pb, lts)
+        medium.append(rec)
+    out["medium_random"] = medium
+
+    with gzip.open(os.path.join(OUT, "cases.json.gz"), "wt") as fh:
+        json.dump(out, fh, separators=(",", ":"))
+    print("wrote cases.json.gz")
+
+
+def sweep(count=1000):
+    """The acceptance sweep generator (test_acceptance.py:114-125,
+    _support.py:55-66) with Priority outputs and observer chains."""
+    pb = _ref()
+    sys.path.insert(0, REF_TESTS)
+    import _support as sup
+    rng = random.Random(20260814)
+    recs = []
+    for idx in range(count):
+        seed = rng.randrange(2 ** 32)
+        lts = sup.random_lts(random.Random(seed))
+        rec = lts_arrays(lts)
+        rec["seed"] = seed
+        rec["bcrp"] = run_bcrp(pb, lts, snaps=True)
+        if len(lts.action_labels) == 1:
+            edges = [(t.source, t.target) for t in lts.transitions]
+            rec["rcpp_trivial"] = run_rcpp(pb, lts.n, edges, [0] * lts.n, snaps=True)
+        recs.append(rec)
+    with gzip.open(os.path.join(OUT, "sweep.json.gz"), "wt") as fh:
+        json.dump(recs, fh, separators=(",", ":"))
+    print(f"wrote sweep.json.gz ({count} instances)")
+
+
+def c1():
+    """n=10k, m=50k, |Act|=4, random.Random(1)."""
+    pb = _ref()
+    n, m = 10_000, 50_000
+    rng = random.Random(1)
+    labels = ["a0", "a1", "a2", "a3"]
+    edges = []
+    for _ in range(m):
+        s = rng.randrange(n)
+        lab = labels[rng.randrange(4)]
+        t = rng.randrange(n)
+        edges.append((s, lab, t))
+    lts = pb.lts_from_labeled_edges(n, edges, extra_labels=labels)
+    t0 = time.perf_counter()
+    res = run_bcrp(pb, lts)
+    res["wall_s"] = time.perf_counter() - t0
+    res["recipe"] = "random.Random(1); per edge: s=randrange(n), lab=labels[randrange(4)], t=randrange(n)"
+    res["n"], res["m"], res["num_actions"] = n, m, 4
+    arrays = lts_arrays(lts)
+    np.savez_compressed(os.path.join(OUT, "c1_reference.npz"),
+                        src=np.array(arrays["src"], np.int32),
+                        act=np.array(arrays["act"], np.int32),
+                        dst=np.array(arrays["dst"], np.int32),
+                        block=np.array(res["block"], np.int32),
+                        splits=np.array(res["splits"], np.int32))
+    meta = {k: v for k, v in res.items() if k not in ("block", "splits")}
+    with open(os.path.join(OUT, "c1_reference.json"), "w") as fh:
+        json.dump(meta, fh, indent=1)
+    print("c1:", meta)
+
+
+if __name__ == "__main__":
+    os.makedirs(OUT, exist_ok=True)
+    what = sys.argv[1] if len(sys.argv) > 1 else "cases"
+    {"cases": cases, "sweep": sweep, "c1": c1}[what]()

@@ -1,0 +1,192 @@
+"""Labelled bisimulation refinement (BCRP, Alg. 3-5) on the B200.
+
+Drop-in for /root/reference/pkg/src/parbisim/bcrp.py: same entry points
+(`bcrp_run`, `preprocess`, `partition_by_outgoing_labels`, `BcrpAux`), same
+arguments, results and exceptions.  The work happens in libbisim.so; this
+module only converts between the reference's types and int32 arrays.
+
+`bcrp_arrays` is the array-level API underneath: numpy columns
+in, the int32 block array plus RunStats out, with no per-transition Python
+objects anywhere.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .lts import Lts, Partition, RunStats, Transition
+from .policy import PolicyViolationError, SuperstepLimitError, policy_kind
+
+
+@dataclass(frozen=True)
+class BcrpAux:
+    """Preprocessing tables (bcrp.py:37-46), in sorted-transition order."""
+
+    lts: Lts
+    action_switch: tuple[int, ...]
+    order: tuple[int, ...]
+    nr_marks: tuple[int, ...]
+    off: tuple[int, ...]
+    mark_length: int
+
+
+def lts_columns(lts) -> tuple[int, np.ndarray, np.ndarray, np.ndarray, int]:
+    """(n, src, act, dst, |Act|) for this package's Lts or any object with the
+    reference Lts attributes (n, action_labels, transitions)."""
+    if isinstance(lts, Lts):
+        s, a, d = lts.columns()
+        return lts.n, s, a, d, len(lts.action_labels)
+    trans = lts.transitions
+    m = len(trans)
+    flat = (np.fromiter((v for t in trans for v in (t[0], t[1], t[2])), dtype=np.int32,
+                        count=3 * m).reshape(m, 3) if m else np.zeros((0, 3), np.int32))
+    cols = [np.ascontiguousarray(flat[:, k]) for k in range(3)]
+    return int(lts.n), cols[0], cols[1], cols[2], len(lts.action_labels)
+
+
+class _ObserverBridge:
+    """Adapts observer(iteration, Partition) to the C callback; an exception
+    raised by the observer aborts the native run and is re-raised here."""
+
+    def __init__(self, observer):
+        self.observer = observer
+        self.exc = None
+
+        def cb(k, block_ptr, n, _user):
+            try:
+                blk = np.ctypeslib.as_array(block_ptr, shape=(n,)).copy()
+                self.observer(int(k), Partition(blk, _trusted=True))
+                return 0
+            except BaseException as e:  # noqa: BLE001 - re-raised below
+                self.exc = e
+                return 1
+
+        self.cfunc = N.OBSERVER(cb)
+
+
+def _options(device: int, mode: int, bridge) -> N.Options:
+    o = N.Options()
+    o.device = device
+    o.mode = mode
+    if bridge is not None:
+        o.observer = bridge.cfunc
+    return o
+
+
+def _raise_for(rc: int, bridge, guard_msg_stats: N.Stats):
+    if rc == N.BISIM_OK:
+        return
+    msg = N.last_error()
+    if rc == N.BISIM_ABORTED and bridge is not None and bridge.exc is not None:
+        raise bridge.exc
+    if rc == N.BISIM_GUARD:
+        raise SuperstepLimitError(msg)
+    if rc == N.BISIM_BAD_INPUT:
+        raise ValueError(msg)
+    raise N.NativeError(rc, msg)
+
+
+def bcrp_arrays(n: int, src, act, dst, num_actions: int, *, max_supersteps: int | None = None,
+                observer=None, device: int = 0, mode: int = N.MODE_AUTO):
+    """Coarsest bisimulation of the LTS given by int32 columns.
+
+    Returns ``(block, RunStats, native_stats)`` where ``block`` is an int32
+    numpy array in canonical leader form.
+    """
+    src, act, dst = N.as_i32(src), N.as_i32(act), N.as_i32(dst)
+    m = src.size
+    guard = N.DEFAULT_GUARD if max_supersteps is None else int(max_supersteps)
+    cap = 3 * n + 16
+    block = np.empty(n, np.int32)
+    splits = np.zeros(cap, np.int32)
+    st = N.Stats()
+    bridge = _ObserverBridge(observer) if observer is not None else None
+    opt = _options(device, N.MODE_STEPPED if observer is not None else mode, bridge)
+    rc = N.lib().bisim_bcrp_ex(n, m, int(num_actions), N.ptr(src), N.ptr(act), N.ptr(dst), guard,
+                               N.ptr(block), N.ptr(splits), cap, ctypes.byref(st),
+                               ctypes.byref(opt))
+    _raise_for(rc, bridge, st)
+    R = int(st.supersteps)
+    stats = RunStats(supersteps=R, splits_per_iteration=tuple(splits[:R].tolist()),
+                     final_block_count=int(st.final_blocks),
+                     initial_block_count=int(st.initial_blocks))
+    return block, stats, st.as_dict()
+
+
+def _check_policy(policy, common_election):
+    kind = policy_kind(policy)
+    if common_election is None:
+        common_election = kind == "common"
+    if kind == "common" and not common_election:
+        # Plain Common (no Alg. 6 election) is illegal as soon as two
+        # processors write different values; the GPU kernels implement the
+        # elected (Priority-equivalent) program only.
+        raise PolicyViolationError("C", [])
+    return kind
+
+
+def bcrp_run(lts, policy, *, common_election: bool | None = None, observer=None,
+             max_supersteps: int | None = None, device: int = 0):
+    """Coarsest strong bisimulation of a labelled system (bcrp.py:192-315).
+
+    Same contract as the reference: returns ``(Partition, RunStats)``;
+    ``observer(iteration, partition)`` is called after every counted
+    superstep; ``max_supersteps`` defaults to ``3n + |Act| + 8`` and raises
+    :class:`SuperstepLimitError` when exceeded.
+    """
+    _check_policy(policy, common_election)
+    n, src, act, dst, A = lts_columns(lts)
+    block, stats, _ = bcrp_arrays(n, src, act, dst, A, max_supersteps=max_supersteps,
+                                  observer=observer, device=device)
+    return Partition(block, _trusted=True), stats
+
+
+def partition_by_outgoing_labels(lts, policy, *, common_election: bool | None = None,
+                                 device: int = 0) -> Partition:
+    """States grouped by outgoing label set, min-index leaders
+    (bcrp.py:129-141)."""
+    _check_policy(policy, common_election)
+    n, src, act, _, A = lts_columns(lts)
+    block = np.empty(n, np.int32)
+    N.check(N.lib().bisim_label_partition(n, src.size, A, N.ptr(src), N.ptr(act), N.ptr(block),
+                                          device))
+    return Partition(block, _trusted=True)
+
+
+def preprocess(lts, device: int = 0) -> BcrpAux:
+    """Label-ordering tables (bcrp.py:116-126).
+
+    order/nr_marks/off/mark_length come from the GPU preprocessing kernels
+    (label masks + slot ranks).  The refinement path never sorts transitions;
+    only this table export arranges them in the reference's stable
+    (source, action) order.
+    """
+    n, src, act, dst, A = lts_columns(lts)
+    m = src.size
+    order = np.empty(max(m, 1), np.int32)
+    nr = np.empty(n, np.int32)
+    off = np.empty(n, np.int32)
+    L = ctypes.c_int64(0)
+    rc = N.lib().bisim_preprocess(n, m, A, N.ptr(src), N.ptr(act), N.ptr(order), N.ptr(nr),
+                                  N.ptr(off), ctypes.byref(L), device)
+    if rc == N.BISIM_BAD_INPUT:
+        raise ValueError(N.last_error())
+    N.check(rc)
+    perm = np.lexsort((act, src)) if m else np.zeros(0, np.int64)  # stable (source, action)
+    s_src, s_act, s_dst = src[perm], act[perm], dst[perm]
+    switch = np.zeros(m, np.int32)
+    if m > 1:
+        switch[1:] = ((s_src[1:] == s_src[:-1]) & (s_act[1:] != s_act[:-1])).astype(np.int32)
+    labels = lts.action_labels
+    sorted_lts = Lts.from_arrays(n, s_src, s_act, s_dst, labels,
+                                 getattr(lts, "initial_state", 0), validate=False)
+    return BcrpAux(lts=sorted_lts, action_switch=tuple(switch.tolist()),
+                   order=tuple(order[:m][perm].tolist()), nr_marks=tuple(nr.tolist()),
+                   off=tuple(off.tolist()), mark_length=int(L.value))
+
+
+__all__ = ["BcrpAux", "bcrp_arrays", "bcrp_run", "partition_by_outgoing_labels", "preprocess",
+           "lts_columns", "Transition"]

@@ -1,0 +1,637 @@
+// capi.cu -- host orchestration and the C ABI of libbisim.so (include/bisim.h).
+//
+// One call = H2D (host entry points only) -> preprocessing kernels -> label
+// pre-partition (cooperative kernel) -> refinement loop (one persistent
+// cooperative kernel, or one launch per round when an observer is attached)
+// -> D2H.  Device buffers live in a per-device context and are reused across
+// calls; every call runs on the context's own stream and is timed with CUDA
+// events on that stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/bisim.h"
+#include "kernels.cuh"
+
+namespace bisim {
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& msg) : std::runtime_error(msg), code(c) {}
+};
+
+#define CK(expr)                                                                         \
+    do {                                                                                 \
+        cudaError_t e_ = (expr);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            throw Error(BISIM_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void* ensure(size_t bytes) {
+        bytes = std::max<size_t>(bytes, 16);
+        if (bytes > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            cap = 0;
+            CK(cudaMalloc(&p, bytes));
+            cap = bytes;
+        }
+        return p;
+    }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+struct Ctx {
+    int device = 0;
+    int sms = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[6] = {};
+    int grid_refine_bcrp = 0, grid_refine_rcpp = 0, grid_label = 0;
+    std::mutex mu;
+    DevBuf src, act, dst, pi0, lmask, off, rev_ptr, cursor, rev_slot, block, nl, mark, unstable,
+        split_list, cmem, splits, ctrl, scan_tmp;
+    int launches = 0;
+};
+
+std::mutex g_ctx_mu;
+std::vector<std::unique_ptr<Ctx>> g_ctx;
+
+int occupancy_grid(const void* fn, int sms) {
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, 0));
+    if (occ < 1) throw Error(BISIM_CUDA, "persistent kernel cannot be resident");
+    return sms * std::min(occ, 2);
+}
+
+Ctx* get_ctx(int device) {
+    std::lock_guard<std::mutex> g(g_ctx_mu);
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+        throw Error(BISIM_CUDA, "no CUDA device available (libbisim has no CPU fallback)");
+    if (device < 0 || device >= count) throw Error(BISIM_CUDA, "invalid CUDA device ordinal");
+    if ((int)g_ctx.size() < count) g_ctx.resize(count);
+    if (!g_ctx[device]) {
+        auto c = std::make_unique<Ctx>();
+        c->device = device;
+        CK(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, device));
+        if (!prop.cooperativeLaunch) throw Error(BISIM_CUDA, "device lacks cooperative launch");
+        c->sms = prop.multiProcessorCount;
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        for (auto& e : c->ev) CK(cudaEventCreate(&e));
+        c->grid_refine_bcrp = occupancy_grid((const void*)k_refine<false>, c->sms);
+        c->grid_refine_rcpp = occupancy_grid((const void*)k_refine<true>, c->sms);
+        c->grid_label = occupancy_grid((const void*)k_label_rounds, c->sms);
+        g_ctx[device] = std::move(c);
+    }
+    return g_ctx[device].get();
+}
+
+int grid_for(int64_t work, int threads, int sms) {
+    const int64_t g = (work + threads - 1) / threads;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)sms * 16));
+}
+
+void scan_excl(Ctx& c, int32_t* d, int64_t N) {
+    // d[0..N) counts -> exclusive prefix, d[N] = total
+    const int64_t ntiles = std::max<int64_t>(1, (N + kScanTile - 1) / kScanTile);
+    int64_t* tiles = (int64_t*)c.scan_tmp.ensure(ntiles * sizeof(int64_t));
+    k_scan_tiles<<<(unsigned)ntiles, kScanThreads, 0, c.stream>>>(d, N, tiles);
+    k_scan_sums<<<1, kScanThreads, 0, c.stream>>>(tiles, ntiles);
+    k_scan_apply<<<(unsigned)ntiles, kScanThreads, 0, c.stream>>>(d, N, tiles);
+    c.launches += 3;
+    CK(cudaGetLastError());
+}
+
+struct Job {
+    bool bcrp = true;
+    int32_t n = 0;
+    int64_t m = 0;
+    int32_t A = 0;
+    const int32_t *src = nullptr, *act = nullptr, *dst = nullptr, *pi0 = nullptr;
+    bool inputs_on_device = false;
+    int64_t max_supersteps = BISIM_DEFAULT_GUARD;
+    int32_t* block_out = nullptr;
+    bool block_out_on_device = false;
+    int32_t* splits_out = nullptr;
+    int64_t splits_cap = 0;
+    bisim_stats* st = nullptr;
+    bisim_options opt{};
+};
+
+template <typename T>
+T* as(DevBuf& b) {
+    return reinterpret_cast<T*>(b.p);
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    return ms;
+}
+
+int run(Job& j) {
+    if (j.n < 1) throw Error(BISIM_BAD_INPUT, "state count must be at least 1");
+    if (j.m < 0 || j.m >= (int64_t)INT32_MAX) throw Error(BISIM_BAD_INPUT, "transition count out of range");
+    if (j.A < 0) throw Error(BISIM_BAD_INPUT, "negative action count");
+    if (j.m > 0 && (!j.src || !j.dst || (j.bcrp && !j.act)))
+        throw Error(BISIM_BAD_INPUT, "null transition array");
+    if (!j.bcrp && !j.pi0) throw Error(BISIM_BAD_INPUT, "null pi0");
+    if (!j.block_out) throw Error(BISIM_BAD_INPUT, "null block_out");
+
+    Ctx& c = *get_ctx(j.opt.device);
+    std::lock_guard<std::mutex> lock(c.mu);
+    CK(cudaSetDevice(c.device));
+    c.launches = 0;
+    cudaStream_t st = c.stream;
+    const int32_t n = j.n;
+    const int64_t m = j.m;
+    const int32_t A = j.bcrp ? j.A : 0;
+    const int32_t W = j.bcrp ? (A + 63) / 64 : 0;
+    const int64_t guard = j.max_supersteps == BISIM_DEFAULT_GUARD
+                              ? (j.bcrp ? 3LL * n + A + 8 : 3LL * n + 9)
+                              : j.max_supersteps;
+    bisim_stats S{};
+    S.label_rounds = A;
+    const bool stepped = j.opt.observer != nullptr || j.opt.mode == BISIM_MODE_STEPPED;
+    S.mode = stepped ? BISIM_MODE_STEPPED : BISIM_MODE_PERSISTENT;
+
+    // ---- buffers
+    const int64_t mm = std::max<int64_t>(m, 1);
+    const int32_t* d_src;
+    const int32_t* d_act = nullptr;
+    const int32_t* d_dst;
+    const int32_t* d_pi0 = nullptr;
+    CK(cudaEventRecord(c.ev[0], st));
+    if (j.inputs_on_device) {
+        d_src = j.src;
+        d_act = j.act;
+        d_dst = j.dst;
+        d_pi0 = j.pi0;
+    } else {
+        d_src = (int32_t*)c.src.ensure(mm * 4);
+        d_dst = (int32_t*)c.dst.ensure(mm * 4);
+        if (m) {
+            CK(cudaMemcpyAsync((void*)d_src, j.src, m * 4, cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync((void*)d_dst, j.dst, m * 4, cudaMemcpyHostToDevice, st));
+        }
+        if (j.bcrp) {
+            d_act = (int32_t*)c.act.ensure(mm * 4);
+            if (m) CK(cudaMemcpyAsync((void*)d_act, j.act, m * 4, cudaMemcpyHostToDevice, st));
+        } else {
+            d_pi0 = (int32_t*)c.pi0.ensure((int64_t)n * 4);
+            CK(cudaMemcpyAsync((void*)d_pi0, j.pi0, (int64_t)n * 4, cudaMemcpyHostToDevice, st));
+        }
+    }
+    CK(cudaEventRecord(c.ev[1], st));
+
+    Ctrl* ctrl = (Ctrl*)c.ctrl.ensure(sizeof(Ctrl));
+    unsigned long long* lmask =
+        j.bcrp ? (unsigned long long*)c.lmask.ensure((size_t)std::max(W, 1) * n * 8) : nullptr;
+    int32_t* off = j.bcrp ? (int32_t*)c.off.ensure(((int64_t)n + 1) * 4) : nullptr;
+    int32_t* rev_ptr = (int32_t*)c.rev_ptr.ensure(((int64_t)n + 1) * 4);
+    int32_t* cursor = (int32_t*)c.cursor.ensure(((int64_t)n + 1) * 4);
+    int32_t* rev_slot = (int32_t*)c.rev_slot.ensure(mm * 4);
+    int32_t* block = (int32_t*)c.block.ensure((int64_t)n * 4);
+    unsigned long long* nl = (unsigned long long*)c.nl.ensure((int64_t)n * 8);
+    const int64_t mark_bits = j.bcrp ? m : n;  // L <= m (bcrp.py:113)
+    uint32_t* mark = (uint32_t*)c.mark.ensure(((mark_bits + 31) / 32 + 2) * 4);
+    const int64_t nwords = ((int64_t)n + 31) / 32;
+    uint32_t* unstable = (uint32_t*)c.unstable.ensure((nwords + 1) * 4);
+    int32_t* split_list = (int32_t*)c.split_list.ensure((int64_t)n * 4);
+    int32_t* cmem = (int32_t*)c.cmem.ensure((int64_t)n * 4);
+    // rounds can never exceed the guard nor the 3n bound of the paper
+    const int64_t splits_dev_cap =
+        std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(guard - A, 1), 3LL * n + 16));
+    int32_t* splits = (int32_t*)c.splits.ensure(splits_dev_cap * 4);
+
+    const int TB = 256;
+    // ---- preprocessing (bcrp.py:49-126)
+    CK(cudaMemsetAsync(ctrl, 0, sizeof(Ctrl), st));
+    if (j.bcrp) {
+        CK(cudaMemsetAsync(lmask, 0, (size_t)std::max(W, 1) * n * 8, st));
+        if (m) {
+            k_label_mask<<<grid_for(m, TB, c.sms), TB, 0, st>>>(n, m, A, d_src, d_act, d_dst, lmask, ctrl);
+            ++c.launches;
+        }
+        k_nr_marks<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, W, lmask, off);
+        ++c.launches;
+        scan_excl(c, off, n);
+    } else {
+        if (m) {
+            k_check_edges<<<grid_for(m, TB, c.sms), TB, 0, st>>>(n, m, d_src, d_dst, ctrl);
+            ++c.launches;
+        }
+        k_check_pi0<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, d_pi0, ctrl);
+        ++c.launches;
+    }
+    CK(cudaMemsetAsync(rev_ptr, 0, ((int64_t)n + 1) * 4, st));
+    if (m) {
+        k_indeg<<<grid_for(m, TB, c.sms), TB, 0, st>>>(m, d_dst, rev_ptr);
+        ++c.launches;
+    }
+    scan_excl(c, rev_ptr, n);
+    CK(cudaMemcpyAsync(cursor, rev_ptr, ((int64_t)n + 1) * 4, cudaMemcpyDeviceToDevice, st));
+    if (m) {
+        if (j.bcrp)
+            k_rev_fill<true><<<grid_for(m, TB, c.sms), TB, 0, st>>>(n, m, d_src, d_act, d_dst, lmask, off,
+                                                                 cursor, rev_slot);
+        else
+            k_rev_fill<false><<<grid_for(m, TB, c.sms), TB, 0, st>>>(n, m, d_src, d_act, d_dst, lmask, off,
+                                                                  cursor, rev_slot);
+        ++c.launches;
+    }
+    CK(cudaGetLastError());
+    Ctrl hc;
+    CK(cudaMemcpyAsync(&hc, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+    int32_t L32 = n;
+    if (j.bcrp) CK(cudaMemcpyAsync(&L32, off + n, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(c.ev[2], st));
+    CK(cudaStreamSynchronize(st));
+    if (hc.bad)
+        throw Error(BISIM_BAD_INPUT, j.bcrp ? "transition mentions a state or action outside range"
+                                            : "edge outside 0..n-1 or pi0 is not a leader-form partition");
+    S.mark_length = L32;
+
+    // ---- label pre-partition (bcrp.py:144-184) / pi0 (rcpp.py:58-72)
+    if (j.bcrp && A > 0 && guard < A) {
+        S.guard_count = std::max<int64_t>(guard + 1, 1);
+        *j.st = S;
+        throw Error(BISIM_GUARD, "superstep guard exceeded during the label pre-partition");
+    }
+    CK(cudaMemsetAsync(nl, 0, (int64_t)n * 8, st));
+    if (j.bcrp) {
+        CK(cudaMemsetAsync(block, 0, (int64_t)n * 4, st));
+        if (A > 0) {
+            int32_t nn = n, AA = A;
+            const unsigned long long* lm = lmask;
+            void* args[] = {&nn, &AA, (void*)&lm, &block, &nl};
+            CK(cudaLaunchCooperativeKernel((const void*)k_label_rounds, c.grid_label, kThreads, args, 0, st));
+            ++c.launches;
+        }
+    } else {
+        CK(cudaMemcpyAsync(block, d_pi0, (int64_t)n * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    CK(cudaMemsetAsync(unstable, 0, (nwords + 1) * 4, st));
+    k_init_unstable<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, block, unstable);
+    k_count_leaders<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, block, ctrl);
+    c.launches += 2;
+    CK(cudaMemcpyAsync(&hc, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemsetAsync(mark, 0, ((mark_bits + 31) / 32 + 2) * 4, st));
+    CK(cudaMemsetAsync(splits, 0, splits_dev_cap * 4, st));
+    CK(cudaEventRecord(c.ev[3], st));
+    CK(cudaStreamSynchronize(st));
+    S.initial_blocks = hc.count;
+
+    // ---- refinement loop
+    LoopParams lp{};
+    lp.n = n;
+    lp.A = A;
+    lp.reflag_c = j.bcrp ? 1 : 0;
+    lp.has_guard = 1;
+    lp.max_supersteps = guard;
+    lp.round_limit = stepped ? 1 : INT64_MAX;
+    lp.splits_cap = splits_dev_cap;
+    lp.off = off;
+    lp.rev_ptr = rev_ptr;
+    lp.rev_slot = rev_slot;
+    lp.block = block;
+    lp.nl = nl;
+    lp.mark = mark;
+    lp.unstable = unstable;
+    lp.split_list = split_list;
+    lp.cmem = cmem;
+    lp.splits = splits;
+    lp.ctrl = ctrl;
+    const void* kfn = j.bcrp ? (const void*)k_refine<false> : (const void*)k_refine<true>;
+    const int kgrid = j.bcrp ? c.grid_refine_bcrp : c.grid_refine_rcpp;
+    void* kargs[] = {&lp};
+    std::vector<int32_t> host_block;
+    int64_t rounds = 0;
+    int rc = BISIM_OK;
+    for (;;) {
+        k_ctrl_reset<<<1, 1, 0, st>>>(ctrl);
+        CK(cudaLaunchCooperativeKernel(kfn, kgrid, kThreads, kargs, 0, st));
+        c.launches += 2;
+        if (!stepped) break;
+        CK(cudaMemcpyAsync(&hc, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (hc.error || hc.done) break;
+        if (hc.round > rounds) {
+            rounds = hc.round;
+            if (j.opt.observer) {
+                host_block.resize(n);
+                CK(cudaMemcpyAsync(host_block.data(), block, (int64_t)n * 4, cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                if (j.opt.observer(rounds, host_block.data(), n, j.opt.observer_user) != 0) {
+                    rc = BISIM_ABORTED;
+                    break;
+                }
+            }
+        }
+    }
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c.ev[4], st));
+    CK(cudaMemcpyAsync(&hc, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    S.supersteps = hc.round;
+    if (rc == BISIM_ABORTED) {
+        *j.st = S;
+        throw Error(BISIM_ABORTED, "observer aborted the run");
+    }
+    if (hc.error == BISIM_GUARD) {
+        S.guard_count = hc.guard_count;
+        *j.st = S;
+        throw Error(BISIM_GUARD, "superstep guard exceeded (" + std::to_string(hc.guard_count) + " > " +
+                                     std::to_string(guard) + ")");
+    }
+
+    // ---- results
+    CK(cudaMemsetAsync(&ctrl->count, 0, 4, st));
+    k_count_leaders<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, block, ctrl);
+    ++c.launches;
+    if (j.block_out_on_device)
+        CK(cudaMemcpyAsync(j.block_out, block, (int64_t)n * 4, cudaMemcpyDeviceToDevice, st));
+    else
+        CK(cudaMemcpyAsync(j.block_out, block, (int64_t)n * 4, cudaMemcpyDeviceToHost, st));
+    const int64_t R = hc.round;
+    const int64_t ncopy = std::min<int64_t>(std::min<int64_t>(R, j.splits_cap), splits_dev_cap);
+    if (j.splits_out && ncopy > 0)
+        CK(cudaMemcpyAsync(j.splits_out, splits, ncopy * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&hc, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(c.ev[5], st));
+    CK(cudaStreamSynchronize(st));
+    S.final_blocks = hc.count;
+    S.t_h2d_ms = elapsed(c.ev[0], c.ev[1]);
+    S.t_pre_ms = elapsed(c.ev[1], c.ev[2]);
+    S.t_label_ms = elapsed(c.ev[2], c.ev[3]);
+    S.t_alg_ms = elapsed(c.ev[3], c.ev[4]);
+    S.t_d2h_ms = elapsed(c.ev[4], c.ev[5]);
+    // Algorithmic bytes of the loop: per round the
+    // dense state scans (block twice, slot offsets, leader offsets, mark
+    // words, unstable bitmap) plus per in-edge of C a slot read and a mark
+    // word set and clear, plus per split state block/new-leader traffic.
+    const int64_t per_round = j.bcrp ? (int64_t)n * (4 + 4 + 4 + 4 + 4) + (int64_t)L32 / 8 * 2 + nwords * 4
+                                     : (int64_t)n * (4 + 4) + nwords * 4 * 3;
+    S.bytes_alg = (R + 1) * per_round + (int64_t)hc.work_edges * (4 + 4 + 4 + 4) +
+                  (int64_t)hc.work_splits * (4 + 4 + 8 + 4 + 8);
+    S.kernel_launches = c.launches;
+    *j.st = S;
+    return BISIM_OK;
+}
+
+int guarded(Job& j) {
+    bisim_stats dummy{};
+    if (!j.st) j.st = &dummy;
+    try {
+        g_last_error.clear();
+        return run(j);
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return BISIM_CUDA;
+    }
+}
+
+bisim_options opts_or_default(const bisim_options* o, int device) {
+    bisim_options r{};
+    if (o) r = *o;
+    else r.device = device;
+    return r;
+}
+
+}  // namespace
+}  // namespace bisim
+
+using namespace bisim;
+
+extern "C" {
+
+int bisim_bcrp_ex(int32_t n, int64_t m, int32_t num_actions, const int32_t* src, const int32_t* act,
+                  const int32_t* dst, int64_t max_supersteps, int32_t* block_out, int32_t* splits_out,
+                  int64_t splits_cap, bisim_stats* st, const bisim_options* opt) {
+    Job j;
+    j.bcrp = true;
+    j.n = n;
+    j.m = m;
+    j.A = num_actions;
+    j.src = src;
+    j.act = act;
+    j.dst = dst;
+    j.max_supersteps = max_supersteps;
+    j.block_out = block_out;
+    j.splits_out = splits_out;
+    j.splits_cap = splits_cap;
+    j.st = st;
+    j.opt = opts_or_default(opt, 0);
+    return guarded(j);
+}
+
+int bisim_bcrp(int32_t n, int64_t m, int32_t num_actions, const int32_t* src, const int32_t* act,
+               const int32_t* dst, int64_t max_supersteps, int32_t* block_out, int32_t* splits_out,
+               int64_t splits_cap, bisim_stats* st, int device) {
+    bisim_options o{};
+    o.device = device;
+    return bisim_bcrp_ex(n, m, num_actions, src, act, dst, max_supersteps, block_out, splits_out, splits_cap,
+                         st, &o);
+}
+
+int bisim_rcpp_ex(int32_t n, int64_t m, const int32_t* src, const int32_t* dst, const int32_t* pi0_leader,
+                  int64_t max_supersteps, int32_t* block_out, int32_t* splits_out, int64_t splits_cap,
+                  bisim_stats* st, const bisim_options* opt) {
+    Job j;
+    j.bcrp = false;
+    j.n = n;
+    j.m = m;
+    j.src = src;
+    j.dst = dst;
+    j.pi0 = pi0_leader;
+    j.max_supersteps = max_supersteps;
+    j.block_out = block_out;
+    j.splits_out = splits_out;
+    j.splits_cap = splits_cap;
+    j.st = st;
+    j.opt = opts_or_default(opt, 0);
+    return guarded(j);
+}
+
+int bisim_rcpp(int32_t n, int64_t m, const int32_t* src, const int32_t* dst, const int32_t* pi0_leader,
+               int64_t max_supersteps, int32_t* block_out, int32_t* splits_out, int64_t splits_cap,
+               bisim_stats* st, int device) {
+    bisim_options o{};
+    o.device = device;
+    return bisim_rcpp_ex(n, m, src, dst, pi0_leader, max_supersteps, block_out, splits_out, splits_cap, st,
+                         &o);
+}
+
+int bisim_bcrp_device(int32_t n, int64_t m, int32_t num_actions, const int32_t* d_src, const int32_t* d_act,
+                      const int32_t* d_dst, int64_t max_supersteps, int32_t* d_block_out, int32_t* splits_out,
+                      int64_t splits_cap, bisim_stats* st, const bisim_options* opt) {
+    Job j;
+    j.bcrp = true;
+    j.n = n;
+    j.m = m;
+    j.A = num_actions;
+    j.src = d_src;
+    j.act = d_act;
+    j.dst = d_dst;
+    j.inputs_on_device = true;
+    j.max_supersteps = max_supersteps;
+    j.block_out = d_block_out;
+    j.block_out_on_device = true;
+    j.splits_out = splits_out;
+    j.splits_cap = splits_cap;
+    j.st = st;
+    j.opt = opts_or_default(opt, 0);
+    return guarded(j);
+}
+
+int bisim_rcpp_device(int32_t n, int64_t m, const int32_t* d_src, const int32_t* d_dst,
+                      const int32_t* d_pi0_leader, int64_t max_supersteps, int32_t* d_block_out,
+                      int32_t* splits_out, int64_t splits_cap, bisim_stats* st, const bisim_options* opt) {
+    Job j;
+    j.bcrp = false;
+    j.n = n;
+    j.m = m;
+    j.src = d_src;
+    j.dst = d_dst;
+    j.pi0 = d_pi0_leader;
+    j.inputs_on_device = true;
+    j.max_supersteps = max_supersteps;
+    j.block_out = d_block_out;
+    j.block_out_on_device = true;
+    j.splits_out = splits_out;
+    j.splits_cap = splits_cap;
+    j.st = st;
+    j.opt = opts_or_default(opt, 0);
+    return guarded(j);
+}
+
+int bisim_preprocess(int32_t n, int64_t m, int32_t num_actions, const int32_t* src, const int32_t* act,
+                     int32_t* order_out, int32_t* nr_marks_out, int32_t* off_out, int64_t* mark_length,
+                     int device) {
+    try {
+        g_last_error.clear();
+        if (n < 1 || m < 0 || m >= (int64_t)INT32_MAX || num_actions < 0)
+            throw Error(BISIM_BAD_INPUT, "bad sizes");
+        Ctx& c = *get_ctx(device);
+        std::lock_guard<std::mutex> lock(c.mu);
+        CK(cudaSetDevice(c.device));
+        cudaStream_t st = c.stream;
+        const int64_t mm = std::max<int64_t>(m, 1);
+        const int32_t W = (num_actions + 63) / 64;
+        int32_t* d_src = (int32_t*)c.src.ensure(mm * 4);
+        int32_t* d_act = (int32_t*)c.act.ensure(mm * 4);
+        int32_t* d_order = (int32_t*)c.rev_slot.ensure(mm * 4);
+        Ctrl* ctrl = (Ctrl*)c.ctrl.ensure(sizeof(Ctrl));
+        auto* lmask = (unsigned long long*)c.lmask.ensure((size_t)std::max(W, 1) * n * 8);
+        int32_t* off = (int32_t*)c.off.ensure(((int64_t)n + 1) * 4);
+        if (m) {
+            CK(cudaMemcpyAsync(d_src, src, m * 4, cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(d_act, act, m * 4, cudaMemcpyHostToDevice, st));
+        }
+        CK(cudaMemsetAsync(ctrl, 0, sizeof(Ctrl), st));
+        CK(cudaMemsetAsync(lmask, 0, (size_t)std::max(W, 1) * n * 8, st));
+        const int TB = 256;
+        if (m) k_label_mask<<<grid_for(m, TB, c.sms), TB, 0, st>>>(n, m, num_actions, d_src, d_act, d_src, lmask, ctrl);
+        k_nr_marks<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, W, lmask, off);
+        if (nr_marks_out) CK(cudaMemcpyAsync(nr_marks_out, off, (int64_t)n * 4, cudaMemcpyDeviceToHost, st));
+        scan_excl(c, off, n);
+        if (m) k_order<<<grid_for(m, TB, c.sms), TB, 0, st>>>(n, m, d_src, d_act, lmask, d_order);
+        CK(cudaGetLastError());
+        Ctrl hc;
+        int32_t L32 = 0;
+        CK(cudaMemcpyAsync(&hc, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&L32, off + n, 4, cudaMemcpyDeviceToHost, st));
+        if (off_out) CK(cudaMemcpyAsync(off_out, off, (int64_t)n * 4, cudaMemcpyDeviceToHost, st));
+        if (order_out && m) CK(cudaMemcpyAsync(order_out, d_order, m * 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (hc.bad) throw Error(BISIM_BAD_INPUT, "transition mentions a state or action outside range");
+        if (mark_length) *mark_length = L32;
+        return BISIM_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return BISIM_CUDA;
+    }
+}
+
+int bisim_label_partition(int32_t n, int64_t m, int32_t num_actions, const int32_t* src, const int32_t* act,
+                          int32_t* block_out, int device) {
+    // The label partition is the pi0 of a BCRP run; run a BCRP job with a
+    // guard of exactly |Act| so the main loop never starts, and read pi0.
+    try {
+        g_last_error.clear();
+        std::vector<int32_t> dst(std::max<int64_t>(m, 1), 0);
+        Job j;
+        j.bcrp = true;
+        j.n = n;
+        j.m = m;
+        j.A = num_actions;
+        j.src = src;
+        j.act = act;
+        j.dst = m ? src : nullptr;  // targets are irrelevant for the label rounds
+        j.max_supersteps = num_actions;  // main loop's first superstep trips the guard
+        j.block_out = block_out;
+        j.opt.device = device;
+        bisim_stats S{};
+        j.st = &S;
+        try {
+            run(j);
+        } catch (const Error& e) {
+            if (e.code != BISIM_GUARD || S.guard_count != (int64_t)num_actions + 1) throw;
+        }
+        // block buffer holds pi0: the guard fired before any round ran
+        Ctx& c = *get_ctx(device);
+        std::lock_guard<std::mutex> lock(c.mu);
+        CK(cudaMemcpy(block_out, c.block.p, (int64_t)n * 4, cudaMemcpyDeviceToHost));
+        return BISIM_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return BISIM_CUDA;
+    }
+}
+
+const char* bisim_last_error(void) { return g_last_error.c_str(); }
+
+int bisim_device_count(void) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
+    return c;
+}
+
+void* bisim_stream(int device) {
+    try {
+        return (void*)get_ctx(device)->stream;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return nullptr;
+    }
+}
+
+const char* bisim_version(void) { return "libbisim 0.1 (sm_100a, dense persistent loop)"; }
+
+}  // extern "C"

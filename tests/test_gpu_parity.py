@@ -1,0 +1,275 @@
+"""Parity of the CUDA path (libbisim.so through the C ABI) with the reference.
+
+Bit-exact comparisons: block arrays (leader form), supersteps,
+splits_per_iteration, initial/final block counts, per-round observer
+snapshots, guard behaviour.  Small cases compare against fixtures made by
+the unmodified reference (tests/golden/); larger ones against the CPU oracle
+(oracle/bisim_oracle.c, itself pinned to the reference in
+test_oracle_golden.py); full-size configs through exact properties
+(lifted-quotient ground truth, chain round counts, stability).
+"""
+import numpy as np
+import pytest
+
+import _golden as G
+from oracle import oracle
+from paper_2105_11788_b200 import bcrp_arrays, rcpp_arrays
+from paper_2105_11788_b200 import workloads as W
+from paper_2105_11788_b200.policy import SuperstepLimitError
+
+pytestmark = pytest.mark.gpu
+
+
+def _same(block, stats, exp, what):
+    assert list(block) == exp["block"], what
+    assert stats.supersteps == exp["supersteps"], what
+    assert list(stats.splits_per_iteration) == exp["splits"], what
+    assert stats.initial_block_count == exp["initial_blocks"], what
+    assert stats.final_block_count == exp["final_blocks"], what
+
+
+def _same_oracle(block, stats, res, what):
+    assert np.array_equal(block, res.block), what
+    assert stats.supersteps == res.supersteps, what
+    assert np.array_equal(np.asarray(stats.splits_per_iteration, np.int32), res.splits), what
+    assert stats.initial_block_count == res.initial_blocks, what
+    assert stats.final_block_count == res.final_blocks, what
+
+
+class Recorder:
+    def __init__(self):
+        self.chain = []
+
+    def __call__(self, k, part):
+        assert k == len(self.chain) + 1
+        self.chain.append(list(part.block))
+
+
+# ---------------------------------------------------------------- golden
+
+@pytest.mark.parametrize("name", ["pre_fig2", "pre_no_outgoing", "pre_stable_sort"])
+def test_small_labelled_golden(name):
+    rec = G.cases()[name]
+    n, src, act, dst, A = G.arrays(rec)
+    block, st, _ = bcrp_arrays(n, src, act, dst, A)
+    _same(block, st, rec["bcrp"], name)
+    rec_obs = Recorder()
+    block2, st2, _ = bcrp_arrays(n, src, act, dst, A, observer=rec_obs)
+    _same(block2, st2, rec["bcrp"], name + " stepped")
+    assert rec_obs.chain == rec["bcrp"]["snapshots"]
+
+
+def test_five_state_golden():
+    rec = G.cases()["five_state"]
+    obs = Recorder()
+    block, st, _ = rcpp_arrays(5, rec["src"], rec["dst"], rec["pi0"], observer=obs)
+    assert tuple(block) == (0, 1, 2, 3, 3)          # FIVE_STATE_FINAL
+    _same(block, st, rec["rcpp"], "five_state")
+    assert obs.chain == rec["rcpp"]["snapshots"]
+    block, st, _ = rcpp_arrays(5, rec["src"], rec["dst"], rec["pi0"])
+    _same(block, st, rec["rcpp"], "five_state persistent")
+
+
+def test_edge_free():
+    rec = G.cases()["edge_free_4"]
+    n, src, act, dst, A = G.arrays(rec)
+    block, st, _ = rcpp_arrays(n, src, dst, [0] * n)
+    assert st.supersteps == 1 and st.splits_per_iteration == (0,)
+    _same(block, st, rec["rcpp_trivial"], "edge-free rcpp")
+    block, st, _ = bcrp_arrays(n, src, act, dst, A)
+    _same(block, st, rec["bcrp"], "edge-free bcrp")
+
+
+@pytest.mark.parametrize("n", list(range(3, 65)) + [100, 200])
+def test_fanout_family(n):
+    rec = G.cases()[f"fanout_{n}"]
+    nn, src, act, dst, A = G.arrays(rec)
+    block, st, _ = bcrp_arrays(nn, src, act, dst, A)
+    _same(block, st, rec["bcrp"], f"fanout {n}")
+    block, st, _ = rcpp_arrays(nn, src, dst, [0] * nn)
+    _same(block, st, rec["rcpp_trivial"], f"fanout {n} rcpp")
+    if rec["bcrp"].get("snapshots") is not None:
+        obs = Recorder()
+        bcrp_arrays(nn, src, act, dst, A, observer=obs)
+        assert obs.chain == rec["bcrp"]["snapshots"]
+
+
+@pytest.mark.parametrize("n", [2, 3, 10, 100, 200])
+def test_chain_golden(n):
+    rec = G.cases()[f"chain_{n}"]
+    nn, src, act, dst, A = G.arrays(rec)
+    block, st, _ = bcrp_arrays(nn, src, act, dst, A)
+    _same(block, st, rec["bcrp"], f"chain {n}")
+    block, st, _ = rcpp_arrays(nn, src, dst, [0] * nn)
+    _same(block, st, rec["rcpp_trivial"], f"chain {n} rcpp")
+
+
+def test_guard_boundaries():
+    for g in G.cases()["guard"]:
+        rec = G.cases()[g["instance"]]
+        n, src, act, dst, A = G.arrays(rec)
+        exp = g["result"]
+        try:
+            if g["kind"] == "bcrp":
+                block, st, _ = bcrp_arrays(n, src, act, dst, A, max_supersteps=g["max_supersteps"])
+            else:
+                block, st, _ = rcpp_arrays(n, src, dst, [0] * n, max_supersteps=g["max_supersteps"])
+        except SuperstepLimitError:
+            assert exp["guard"], g
+            continue
+        assert not exp["guard"], g
+        _same(block, st, exp, str(g))
+
+
+def test_rcpp_noncanonical_pi0():
+    for i, rec in enumerate(G.cases()["rcpp_noncanonical"]):
+        obs = Recorder()
+        block, st, _ = rcpp_arrays(rec["n"], rec["src"], rec["dst"], rec["pi0"], observer=obs)
+        _same(block, st, rec["rcpp"], f"noncanonical {i}")
+        assert obs.chain == rec["rcpp"]["snapshots"]
+        block, st, _ = rcpp_arrays(rec["n"], rec["src"], rec["dst"], rec["pi0"])
+        _same(block, st, rec["rcpp"], f"noncanonical {i} persistent")
+
+
+def test_medium_random_golden():
+    for i, rec in enumerate(G.cases()["medium_random"]):
+        n, src, act, dst, A = G.arrays(rec)
+        block, st, _ = bcrp_arrays(n, src, act, dst, A)
+        _same(block, st, rec["bcrp"], f"medium {i}")
+
+
+def test_acceptance_sweep():
+    """The reference acceptance sweep's 1000 instances (test_acceptance.py:114-195)."""
+    for rec in G.sweep():
+        n, src, act, dst, A = G.arrays(rec)
+        block, st, _ = bcrp_arrays(n, src, act, dst, A)
+        _same(block, st, rec["bcrp"], f"seed {rec['seed']}")
+        if "rcpp_trivial" in rec:
+            block, st, _ = rcpp_arrays(n, src, dst, [0] * n)
+            _same(block, st, rec["rcpp_trivial"], f"seed {rec['seed']} rcpp")
+
+
+def test_acceptance_sweep_observer_chains():
+    for rec in G.sweep()[:200]:
+        n, src, act, dst, A = G.arrays(rec)
+        obs = Recorder()
+        bcrp_arrays(n, src, act, dst, A, observer=obs)
+        assert obs.chain == rec["bcrp"]["snapshots"], rec["seed"]
+
+
+def test_c1_full_reference_run():
+    """Config c1 (n=10k, m=50k, |Act|=4): the reference's own 2009 s run."""
+    got = G.c1()
+    if got is None:
+        pytest.skip("c1 fixture not generated")
+    meta, z = got
+    block, st, _ = bcrp_arrays(meta["n"], z["src"], z["act"], z["dst"], meta["num_actions"])
+    assert np.array_equal(block, z["block"])
+    assert np.array_equal(np.asarray(st.splits_per_iteration, np.int32), z["splits"])
+    assert st.supersteps == meta["supersteps"] == 13962
+    assert st.final_block_count == meta["final_blocks"] == 9938
+
+
+# ---------------------------------------------------------------- oracle
+
+@pytest.mark.parametrize("n,m,A,seed", [(2000, 10000, 4, 11), (5000, 20000, 3, 12),
+                                        (3000, 30000, 40, 13), (4000, 8000, 1, 14),
+                                        (1000, 50000, 100, 15)])
+def test_random_bcrp_vs_oracle(n, m, A, seed):
+    g = np.random.default_rng(seed)
+    src = g.integers(0, n, m, dtype=np.int32)
+    act = g.integers(0, A, m, dtype=np.int32)
+    dst = g.integers(0, n, m, dtype=np.int32)
+    res = oracle.bcrp(n, src, act, dst, A, threads=4)
+    block, st, _ = bcrp_arrays(n, src, act, dst, A)
+    _same_oracle(block, st, res, f"random {seed}")
+
+
+@pytest.mark.parametrize("n,deg,seed", [(3000, 5, 21), (10000, 3, 22), (2000, 1, 23)])
+def test_random_rcpp_vs_oracle(n, deg, seed):
+    inst = W.c2_kripke(n=n, out_degree=deg, seed=seed)
+    res = oracle.rcpp(n, inst.src, inst.dst, inst.pi0, threads=4)
+    block, st, _ = rcpp_arrays(n, inst.src, inst.dst, inst.pi0)
+    _same_oracle(block, st, res, f"kripke {seed}")
+
+
+def test_hub_heavy_vs_oracle():
+    """Fan-out hubs scaled up: two states with out-degree n, one big block."""
+    inst = W.fanout(3000)
+    res = oracle.bcrp(inst.n, inst.src, inst.act, inst.dst, inst.num_actions, threads=4)
+    block, st, _ = bcrp_arrays(inst.n, inst.src, inst.act, inst.dst, inst.num_actions)
+    _same_oracle(block, st, res, "fanout 3000")
+
+
+def test_many_labels_vs_oracle():
+    """|Act| > 64 exercises multi-word label masks and multi-word slot compares."""
+    inst = W.lifted_quotient(6000, 300, 300, templates=5, labels_per_template=70,
+                             edges_per_label=1, seed=5)
+    res = oracle.bcrp(inst.n, inst.src, inst.act, inst.dst, inst.num_actions, threads=4)
+    block, st, _ = bcrp_arrays(inst.n, inst.src, inst.act, inst.dst, inst.num_actions)
+    _same_oracle(block, st, res, "many labels")
+    assert np.array_equal(block, inst.truth)
+
+
+# ---------------------------------------------------------------- full-size configs
+
+def test_c3_chain_full():
+    inst = W.chain(200_000)
+    block, st, _ = bcrp_arrays(inst.n, inst.src, inst.act, inst.dst, 1)
+    assert st.supersteps == 2 * inst.n - 2
+    assert np.array_equal(block, inst.truth)
+
+
+def _prefix_parity(run_gpu, run_oracle, K):
+    """First K rounds: GPU stepped-mode observer snapshots and per-round
+    split counts equal the oracle's truncated trace."""
+    snaps = []
+
+    class Stop(Exception):
+        pass
+
+    def grab(k, part):
+        snaps.append(np.asarray(part.block, np.int32))
+        if k == K:
+            raise Stop
+
+    with pytest.raises(Stop):
+        run_gpu(grab)
+    res = run_oracle(K)
+    assert res.supersteps == K
+    assert len(snaps) == K
+    for k in range(K):
+        assert np.array_equal(snaps[k], res.snapshots[k]), f"round {k + 1}"
+    return res
+
+
+def test_c2_kripke_prefix_and_final():
+    """c2 at full size (n=1M, m=5M): first 30 rounds bit-exact vs the oracle,
+    final partition equal to the signature-refinement truth."""
+    inst = W.c2_kripke()
+    _prefix_parity(lambda obs: rcpp_arrays(inst.n, inst.src, inst.dst, inst.pi0, observer=obs),
+                   lambda K: oracle.rcpp(inst.n, inst.src, inst.dst, inst.pi0, snap_rounds=K,
+                                         stop_after=K, threads=8), 30)
+    block, st, _ = rcpp_arrays(inst.n, inst.src, inst.dst, inst.pi0)
+    truth = W.signature_bisim(inst.n, inst.src, np.zeros(inst.m, np.int32), inst.dst,
+                              init=inst.pi0)
+    assert np.array_equal(block, truth)
+    assert st.final_block_count == len(np.unique(truth))
+    assert st.supersteps <= 2 * inst.n - st.initial_block_count
+
+
+def test_c4_lifted_prefix():
+    inst = W.c4_lifted(n=1_000_000, k=10_000)
+    _prefix_parity(lambda obs: bcrp_arrays(inst.n, inst.src, inst.act, inst.dst,
+                                           inst.num_actions, observer=obs),
+                   lambda K: oracle.bcrp(inst.n, inst.src, inst.act, inst.dst, inst.num_actions,
+                                         snap_rounds=K, stop_after=K, threads=8), 10)
+    block, st, _ = bcrp_arrays(inst.n, inst.src, inst.act, inst.dst, inst.num_actions)
+    assert np.array_equal(block, inst.truth)
+
+
+def test_c5_vlts_lifted_truth():
+    inst = W.c5_vlts(n=2_000_000, k=1_000, seed=3)
+    block, st, ns = bcrp_arrays(inst.n, inst.src, inst.act, inst.dst, inst.num_actions)
+    assert np.array_equal(block, inst.truth)
+    assert st.final_block_count == len(np.unique(inst.truth))
