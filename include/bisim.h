@@ -55,8 +55,9 @@ extern "C" {
 
 /* Execution strategies of the refinement loop. */
 #define BISIM_MODE_AUTO 0
-#define BISIM_MODE_PERSISTENT 1 /* one cooperative kernel runs every round */
+#define BISIM_MODE_PERSISTENT 1 /* one cooperative kernel runs every round (work-efficient) */
 #define BISIM_MODE_STEPPED 2    /* one launch per round (observer support) */
+#define BISIM_MODE_DENSE 3      /* persistent, every round scans all n states */
 
 typedef struct bisim_stats {
     int64_t supersteps;      /* RunStats.supersteps */

@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libbisim.so")
 
 BISIM_OK, BISIM_BAD_INPUT, BISIM_GUARD, BISIM_CUDA, BISIM_ABORTED = 0, 1, 2, 3, 4
 DEFAULT_GUARD = -(2 ** 63)
-MODE_AUTO, MODE_PERSISTENT, MODE_STEPPED = 0, 1, 2
+MODE_AUTO, MODE_PERSISTENT, MODE_STEPPED, MODE_DENSE = 0, 1, 2, 3
 
 i32p = ctypes.POINTER(ctypes.c_int32)
 OBSERVER = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_int64, i32p, ctypes.c_int32, ctypes.c_void_p)

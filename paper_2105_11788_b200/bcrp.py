@@ -104,7 +104,7 @@ def bcrp_arrays(n: int, src, act, dst, num_actions: int, *, max_supersteps: int 
     splits = np.zeros(cap, np.int32)
     st = N.Stats()
     bridge = _ObserverBridge(observer) if observer is not None else None
-    opt = _options(device, N.MODE_STEPPED if observer is not None else mode, bridge)
+    opt = _options(device, mode, bridge)  # an observer implies stepped rounds
     rc = N.lib().bisim_bcrp_ex(n, m, int(num_actions), N.ptr(src), N.ptr(act), N.ptr(dst), guard,
                                N.ptr(block), N.ptr(splits), cap, ctypes.byref(st),
                                ctypes.byref(opt))

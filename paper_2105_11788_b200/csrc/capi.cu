@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -19,6 +20,7 @@
 
 #include "../../include/bisim.h"
 #include "kernels.cuh"
+#include "kernels_sparse.cuh"
 
 namespace bisim {
 namespace {
@@ -62,20 +64,22 @@ struct Ctx {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[6] = {};
     int grid_refine_bcrp = 0, grid_refine_rcpp = 0, grid_label = 0;
+    int grid_sparse_bcrp = 0, grid_sparse_rcpp = 0;
     std::mutex mu;
     DevBuf src, act, dst, pi0, lmask, off, rev_ptr, cursor, rev_slot, block, nl, mark, unstable,
-        split_list, cmem, splits, ctrl, scan_tmp;
+        split_list, cmem, splits, ctrl, scan_tmp, rev2, members, bstart, bsize, touched, tblock,
+        small_list, big_list, big_base, tmp, scnt, smin, kcur, scur, counter, brange, bar, trace;
     int launches = 0;
 };
 
 std::mutex g_ctx_mu;
 std::vector<std::unique_ptr<Ctx>> g_ctx;
 
-int occupancy_grid(const void* fn, int sms) {
+int occupancy_grid(const void* fn, int sms, int threads = kThreads, int max_per_sm = 2) {
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, 0));
     if (occ < 1) throw Error(BISIM_CUDA, "persistent kernel cannot be resident");
-    return sms * std::min(occ, 2);
+    return sms * std::min(occ, max_per_sm);
 }
 
 Ctx* get_ctx(int device) {
@@ -98,6 +102,8 @@ Ctx* get_ctx(int device) {
         c->grid_refine_bcrp = occupancy_grid((const void*)k_refine<false>, c->sms);
         c->grid_refine_rcpp = occupancy_grid((const void*)k_refine<true>, c->sms);
         c->grid_label = occupancy_grid((const void*)k_label_rounds, c->sms);
+        c->grid_sparse_bcrp = occupancy_grid((const void*)k_refine_sparse<false>, c->sms, kSparseThreads, 1);
+        c->grid_sparse_rcpp = occupancy_grid((const void*)k_refine_sparse<true>, c->sms, kSparseThreads, 1);
         g_ctx[device] = std::move(c);
     }
     return g_ctx[device].get();
@@ -146,10 +152,38 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
     return ms;
 }
 
+// Status of a refinement-loop launch, mode independent.
+struct LoopStatus {
+    int64_t round = 0;
+    int32_t done = 0, error = 0;
+    int64_t guard_count = 0;
+    unsigned long long work_edges = 0, work_members = 0, work_splits = 0;
+};
+
+// Algorithmic bytes of the refinement loop ("Roofline"): the
+// bytes a round must move at minimum, each element counted once.
+int64_t loop_bytes(bool bcrp, bool dense, int32_t n, int64_t L, int64_t R, const LoopStatus& ls) {
+    const int64_t nwords = ((int64_t)n + 31) / 32;
+    if (dense) {
+        // per round: block[] twice, off[s], off[s+1], off[leader], mark words
+        // of s and leader, unstable scan; per in-edge of C slot + mark set/clear
+        const int64_t per_round = bcrp ? (int64_t)n * 20 + L / 8 * 2 + nwords * 4 : (int64_t)n * 8 + nwords * 12;
+        return (R + 1) * per_round + (int64_t)ls.work_edges * 16 + (int64_t)ls.work_splits * 28;
+    }
+    // per round: C's range and control words; per in-edge of C: the packed
+    // reverse edge, mark and touched read-modify-writes, source block id;
+    // per member of a touched block: member id, touched/mark bits, slot
+    // offsets, compaction write and block id write.
+    const int64_t per_edge = bcrp ? 8 + 8 + 8 + 4 : 4 + 8 + 4;
+    const int64_t per_member = bcrp ? 4 + 4 + 8 + 4 + 4 + 4 : 4 + 4 + 4 + 4;
+    return (R + 1) * 64 + (int64_t)ls.work_edges * per_edge + (int64_t)ls.work_members * per_member;
+}
+
 int run(Job& j) {
     if (j.n < 1) throw Error(BISIM_BAD_INPUT, "state count must be at least 1");
     if (j.m < 0 || j.m >= (int64_t)INT32_MAX) throw Error(BISIM_BAD_INPUT, "transition count out of range");
     if (j.A < 0) throw Error(BISIM_BAD_INPUT, "negative action count");
+    if (j.n >= (1 << 30)) throw Error(BISIM_BAD_INPUT, "state count above 2^30 is not supported");
     if (j.m > 0 && (!j.src || !j.dst || (j.bcrp && !j.act)))
         throw Error(BISIM_BAD_INPUT, "null transition array");
     if (!j.bcrp && !j.pi0) throw Error(BISIM_BAD_INPUT, "null pi0");
@@ -167,12 +201,13 @@ int run(Job& j) {
     const int64_t guard = j.max_supersteps == BISIM_DEFAULT_GUARD
                               ? (j.bcrp ? 3LL * n + A + 8 : 3LL * n + 9)
                               : j.max_supersteps;
+    const bool stepped = j.opt.observer != nullptr || j.opt.mode == BISIM_MODE_STEPPED;
+    const bool dense = j.opt.mode == BISIM_MODE_DENSE;
     bisim_stats S{};
     S.label_rounds = A;
-    const bool stepped = j.opt.observer != nullptr || j.opt.mode == BISIM_MODE_STEPPED;
-    S.mode = stepped ? BISIM_MODE_STEPPED : BISIM_MODE_PERSISTENT;
+    S.mode = stepped ? BISIM_MODE_STEPPED : (dense ? BISIM_MODE_DENSE : BISIM_MODE_PERSISTENT);
 
-    // ---- buffers
+    // ---- inputs
     const int64_t mm = std::max<int64_t>(m, 1);
     const int32_t* d_src;
     const int32_t* d_act = nullptr;
@@ -201,21 +236,18 @@ int run(Job& j) {
     }
     CK(cudaEventRecord(c.ev[1], st));
 
-    Ctrl* ctrl = (Ctrl*)c.ctrl.ensure(sizeof(Ctrl));
+    // ---- buffers
+    Ctrl* ctrl = (Ctrl*)c.ctrl.ensure(std::max(sizeof(Ctrl), sizeof(SCtrl)));
     unsigned long long* lmask =
         j.bcrp ? (unsigned long long*)c.lmask.ensure((size_t)std::max(W, 1) * n * 8) : nullptr;
     int32_t* off = j.bcrp ? (int32_t*)c.off.ensure(((int64_t)n + 1) * 4) : nullptr;
     int32_t* rev_ptr = (int32_t*)c.rev_ptr.ensure(((int64_t)n + 1) * 4);
     int32_t* cursor = (int32_t*)c.cursor.ensure(((int64_t)n + 1) * 4);
-    int32_t* rev_slot = (int32_t*)c.rev_slot.ensure(mm * 4);
     int32_t* block = (int32_t*)c.block.ensure((int64_t)n * 4);
-    unsigned long long* nl = (unsigned long long*)c.nl.ensure((int64_t)n * 8);
     const int64_t mark_bits = j.bcrp ? m : n;  // L <= m (bcrp.py:113)
-    uint32_t* mark = (uint32_t*)c.mark.ensure(((mark_bits + 31) / 32 + 2) * 4);
+    const int64_t mark_words = (mark_bits + 31) / 32 + 2;
+    uint32_t* mark = (uint32_t*)c.mark.ensure(mark_words * 4);
     const int64_t nwords = ((int64_t)n + 31) / 32;
-    uint32_t* unstable = (uint32_t*)c.unstable.ensure((nwords + 1) * 4);
-    int32_t* split_list = (int32_t*)c.split_list.ensure((int64_t)n * 4);
-    int32_t* cmem = (int32_t*)c.cmem.ensure((int64_t)n * 4);
     // rounds can never exceed the guard nor the 3n bound of the paper
     const int64_t splits_dev_cap =
         std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(guard - A, 1), 3LL * n + 16));
@@ -223,7 +255,7 @@ int run(Job& j) {
 
     const int TB = 256;
     // ---- preprocessing (bcrp.py:49-126)
-    CK(cudaMemsetAsync(ctrl, 0, sizeof(Ctrl), st));
+    CK(cudaMemsetAsync(ctrl, 0, std::max(sizeof(Ctrl), sizeof(SCtrl)), st));
     if (j.bcrp) {
         CK(cudaMemsetAsync(lmask, 0, (size_t)std::max(W, 1) * n * 8, st));
         if (m) {
@@ -248,13 +280,22 @@ int run(Job& j) {
     }
     scan_excl(c, rev_ptr, n);
     CK(cudaMemcpyAsync(cursor, rev_ptr, ((int64_t)n + 1) * 4, cudaMemcpyDeviceToDevice, st));
+    int32_t* rev_slot = nullptr;  // dense: slot per in-edge
+    int2* rev2 = nullptr;         // sparse BCRP: (slot, source)
+    int32_t* rev_src = nullptr;   // sparse RCPP: source
+    if (dense) rev_slot = (int32_t*)c.rev_slot.ensure(mm * 4);
+    else if (j.bcrp) rev2 = (int2*)c.rev2.ensure(mm * 8);
+    else rev_src = (int32_t*)c.rev_slot.ensure(mm * 4);
     if (m) {
-        if (j.bcrp)
-            k_rev_fill<true><<<grid_for(m, TB, c.sms), TB, 0, st>>>(n, m, d_src, d_act, d_dst, lmask, off,
-                                                                 cursor, rev_slot);
+        const int g = grid_for(m, TB, c.sms);
+        if (dense && j.bcrp)
+            k_rev_fill<true><<<g, TB, 0, st>>>(n, m, d_src, d_act, d_dst, lmask, off, cursor, rev_slot);
+        else if (dense)
+            k_rev_fill<false><<<g, TB, 0, st>>>(n, m, d_src, d_act, d_dst, lmask, off, cursor, rev_slot);
+        else if (j.bcrp)
+            k_rev_fill2<true><<<g, TB, 0, st>>>(n, m, d_src, d_act, d_dst, lmask, off, cursor, rev2, nullptr);
         else
-            k_rev_fill<false><<<grid_for(m, TB, c.sms), TB, 0, st>>>(n, m, d_src, d_act, d_dst, lmask, off,
-                                                                  cursor, rev_slot);
+            k_rev_fill2<false><<<g, TB, 0, st>>>(n, m, d_src, d_act, d_dst, lmask, off, cursor, nullptr, rev_src);
         ++c.launches;
     }
     CK(cudaGetLastError());
@@ -275,10 +316,11 @@ int run(Job& j) {
         *j.st = S;
         throw Error(BISIM_GUARD, "superstep guard exceeded during the label pre-partition");
     }
-    CK(cudaMemsetAsync(nl, 0, (int64_t)n * 8, st));
+    unsigned long long* nl = (unsigned long long*)c.nl.ensure((int64_t)n * 8);
     if (j.bcrp) {
         CK(cudaMemsetAsync(block, 0, (int64_t)n * 4, st));
         if (A > 0) {
+            CK(cudaMemsetAsync(nl, 0, (int64_t)n * 8, st));
             int32_t nn = n, AA = A;
             const unsigned long long* lm = lmask;
             void* args[] = {&nn, &AA, (void*)&lm, &block, &nl};
@@ -288,53 +330,163 @@ int run(Job& j) {
     } else {
         CK(cudaMemcpyAsync(block, d_pi0, (int64_t)n * 4, cudaMemcpyDeviceToDevice, st));
     }
-    CK(cudaMemsetAsync(unstable, 0, (nwords + 1) * 4, st));
-    k_init_unstable<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, block, unstable);
-    k_count_leaders<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, block, ctrl);
+    // unstable := leaders of the initial partition (level 0 of the set)
+    const int32_t nw0 = (int32_t)nwords, nw1 = (int32_t)((n + 32767) / 32768), nw2 = (int32_t)((n + (1 << 25) - 1) >> 25);
+    uint32_t* U = (uint32_t*)c.unstable.ensure(((int64_t)nw0 + nw1 + nw2 + 3) * 4);
+    CK(cudaMemsetAsync(U, 0, ((int64_t)nw0 + nw1 + nw2 + 3) * 4, st));
+    k_init_unstable<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, block, U);
+    int32_t* leaders = (int32_t*)c.counter.ensure(16);
+    int32_t h_leaders = 0;
+    CK(cudaMemsetAsync(leaders, 0, 4, st));
+    k_count_leaders<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, block, leaders);
     c.launches += 2;
-    CK(cudaMemcpyAsync(&hc, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemsetAsync(mark, 0, ((mark_bits + 31) / 32 + 2) * 4, st));
+    CK(cudaMemcpyAsync(&h_leaders, leaders, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemsetAsync(mark, 0, mark_words * 4, st));
     CK(cudaMemsetAsync(splits, 0, splits_dev_cap * 4, st));
+
+    // ---- loop state
+    SparseParams sp{};
+    LoopParams lp{};
+    if (dense) {
+        int32_t* split_list = (int32_t*)c.split_list.ensure((int64_t)n * 4);
+        int32_t* cmem = (int32_t*)c.cmem.ensure((int64_t)n * 4);
+        CK(cudaMemsetAsync(nl, 0, (int64_t)n * 8, st));
+        lp.n = n;
+        lp.A = A;
+        lp.reflag_c = j.bcrp ? 1 : 0;
+        lp.has_guard = 1;
+        lp.max_supersteps = guard;
+        lp.round_limit = stepped ? 1 : INT64_MAX;
+        lp.splits_cap = splits_dev_cap;
+        lp.off = off;
+        lp.rev_ptr = rev_ptr;
+        lp.rev_slot = rev_slot;
+        lp.block = block;
+        lp.nl = nl;
+        lp.mark = mark;
+        lp.unstable = U;
+        lp.split_list = split_list;
+        lp.cmem = cmem;
+        lp.splits = splits;
+        lp.ctrl = ctrl;
+    } else {
+        // members grouped by block: counting sort of states by label
+        int32_t* members = (int32_t*)c.members.ensure((int64_t)n * 4);
+        int32_t* bstart = (int32_t*)c.bstart.ensure(((int64_t)n + 1) * 4);
+        int32_t* bsize = (int32_t*)c.bsize.ensure((int64_t)n * 4);
+        CK(cudaMemsetAsync(bstart, 0, ((int64_t)n + 1) * 4, st));
+        k_block_sizes<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, block, bstart);
+        ++c.launches;
+        CK(cudaMemcpyAsync(bsize, bstart, (int64_t)n * 4, cudaMemcpyDeviceToDevice, st));
+        scan_excl(c, bstart, n);
+        CK(cudaMemcpyAsync(cursor, bstart, (int64_t)n * 4, cudaMemcpyDeviceToDevice, st));
+        int2* brange = (int2*)c.brange.ensure((int64_t)n * 8);
+        k_pack_ranges<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, bstart, bsize, brange);
+        ++c.launches;
+        k_fill_members<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, block, cursor, members);
+        ++c.launches;
+        uint32_t* U1 = U + nw0;
+        uint32_t* U2 = U1 + nw1 + 1;
+        k_summary<<<grid_for((int64_t)nw1 * 32, TB, c.sms), TB, 0, st>>>(U, nw0, U1, nw1);
+        k_summary<<<1, 64, 0, st>>>(U1, nw1, U2, nw2);
+        c.launches += 2;
+        uint32_t* touched = (uint32_t*)c.touched.ensure((nwords + 2) * 4);
+        uint32_t* tblock = (uint32_t*)c.tblock.ensure((nwords + 2) * 4);
+        CK(cudaMemsetAsync(touched, 0, (nwords + 2) * 4, st));
+        CK(cudaMemsetAsync(tblock, 0, (nwords + 2) * 4, st));
+        sp.n = n;
+        sp.A = A;
+        sp.reflag_c = j.bcrp ? 1 : 0;
+        sp.has_guard = 1;
+        sp.max_supersteps = guard;
+        sp.round_limit = stepped ? 1 : INT64_MAX;
+        sp.splits_cap = splits_dev_cap;
+        sp.off = off;
+        sp.rev_ptr = rev_ptr;
+        sp.rev = rev2;
+        sp.rev_src = rev_src;
+        sp.block = block;
+        sp.members = members;
+        sp.brange = brange;
+        sp.mark = mark;
+        sp.touched = touched;
+        sp.tblock = tblock;
+        sp.U0 = U;
+        sp.U1 = U1;
+        sp.U2 = U2;
+        sp.nw0 = nw0;
+        sp.nw1 = nw1;
+        sp.nw2 = nw2;
+        sp.small_list = (int4*)c.small_list.ensure((int64_t)n * 16);
+        sp.big_list = (int4*)c.big_list.ensure(((int64_t)n / 32 + 2) * 16);
+        sp.big_base = (int32_t*)c.big_base.ensure(((int64_t)n / 32 + 2) * 4);
+        sp.tmp = (int32_t*)c.tmp.ensure((int64_t)n * 4);
+        sp.scnt = (int32_t*)c.scnt.ensure((int64_t)n * 4);
+        sp.smin = (int32_t*)c.smin.ensure((int64_t)n * 4);
+        sp.kcur = (int32_t*)c.kcur.ensure((int64_t)n * 4);
+        sp.scur = (int32_t*)c.scur.ensure((int64_t)n * 4);
+        sp.splits = splits;
+        sp.ctrl = (SCtrl*)ctrl;
+        sp.bar = (GridBarrier*)c.bar.ensure(sizeof(GridBarrier));
+        // developer tracing: BISIM_TRACE=<rounds> BISIM_TRACE_FILE=<path>
+        if (const char* tr = getenv("BISIM_TRACE")) {
+            sp.trace_rounds = atoll(tr);
+            sp.trace = (unsigned long long*)c.trace.ensure(sp.trace_rounds * 64 + 64);
+            CK(cudaMemsetAsync(sp.trace, 0, sp.trace_rounds * 64, st));
+        }
+    }
+    CK(cudaGetLastError());
     CK(cudaEventRecord(c.ev[3], st));
     CK(cudaStreamSynchronize(st));
-    S.initial_blocks = hc.count;
+    S.initial_blocks = h_leaders;
 
     // ---- refinement loop
-    LoopParams lp{};
-    lp.n = n;
-    lp.A = A;
-    lp.reflag_c = j.bcrp ? 1 : 0;
-    lp.has_guard = 1;
-    lp.max_supersteps = guard;
-    lp.round_limit = stepped ? 1 : INT64_MAX;
-    lp.splits_cap = splits_dev_cap;
-    lp.off = off;
-    lp.rev_ptr = rev_ptr;
-    lp.rev_slot = rev_slot;
-    lp.block = block;
-    lp.nl = nl;
-    lp.mark = mark;
-    lp.unstable = unstable;
-    lp.split_list = split_list;
-    lp.cmem = cmem;
-    lp.splits = splits;
-    lp.ctrl = ctrl;
-    const void* kfn = j.bcrp ? (const void*)k_refine<false> : (const void*)k_refine<true>;
-    const int kgrid = j.bcrp ? c.grid_refine_bcrp : c.grid_refine_rcpp;
-    void* kargs[] = {&lp};
+    const void* kfn;
+    int kgrid, kthreads = kThreads;
+    void* kargs[1];
+    if (dense) {
+        kfn = j.bcrp ? (const void*)k_refine<false> : (const void*)k_refine<true>;
+        kgrid = j.bcrp ? c.grid_refine_bcrp : c.grid_refine_rcpp;
+        kargs[0] = &lp;
+    } else {
+        kfn = j.bcrp ? (const void*)k_refine_sparse<false> : (const void*)k_refine_sparse<true>;
+        kgrid = j.bcrp ? c.grid_sparse_bcrp : c.grid_sparse_rcpp;
+        kthreads = kSparseThreads;
+        kargs[0] = &sp;
+    }
+    auto status = [&]() {
+        LoopStatus ls;
+        if (dense) {
+            Ctrl h;
+            CK(cudaMemcpyAsync(&h, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            ls.round = h.round; ls.done = h.done; ls.error = h.error; ls.guard_count = h.guard_count;
+            ls.work_edges = h.work_edges; ls.work_splits = h.work_splits;
+        } else {
+            SCtrl h;
+            CK(cudaMemcpyAsync(&h, ctrl, sizeof(SCtrl), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            ls.round = h.round; ls.done = h.done; ls.error = h.error; ls.guard_count = h.guard_count;
+            ls.work_edges = h.work_edges; ls.work_members = h.work_members;
+        }
+        return ls;
+    };
     std::vector<int32_t> host_block;
     int64_t rounds = 0;
     int rc = BISIM_OK;
     for (;;) {
-        k_ctrl_reset<<<1, 1, 0, st>>>(ctrl);
-        CK(cudaLaunchCooperativeKernel(kfn, kgrid, kThreads, kargs, 0, st));
-        c.launches += 2;
+        if (dense) {
+            k_ctrl_reset<<<1, 1, 0, st>>>(ctrl);
+            ++c.launches;
+        }
+        if (!dense) CK(cudaMemsetAsync(sp.bar, 0, sizeof(GridBarrier), st));
+        CK(cudaLaunchCooperativeKernel(kfn, kgrid, kthreads, kargs, 0, st));
+        ++c.launches;
         if (!stepped) break;
-        CK(cudaMemcpyAsync(&hc, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        if (hc.error || hc.done) break;
-        if (hc.round > rounds) {
-            rounds = hc.round;
+        LoopStatus ls = status();
+        if (ls.error || ls.done) break;
+        if (ls.round > rounds) {
+            rounds = ls.round;
             if (j.opt.observer) {
                 host_block.resize(n);
                 CK(cudaMemcpyAsync(host_block.data(), block, (int64_t)n * 4, cudaMemcpyDeviceToHost, st));
@@ -348,49 +500,55 @@ int run(Job& j) {
     }
     CK(cudaGetLastError());
     CK(cudaEventRecord(c.ev[4], st));
-    CK(cudaMemcpyAsync(&hc, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    S.supersteps = hc.round;
+    LoopStatus ls = status();
+    S.supersteps = ls.round;
     if (rc == BISIM_ABORTED) {
         *j.st = S;
         throw Error(BISIM_ABORTED, "observer aborted the run");
     }
-    if (hc.error == BISIM_GUARD) {
-        S.guard_count = hc.guard_count;
+    if (ls.error == BISIM_GUARD) {
+        S.guard_count = ls.guard_count;
         *j.st = S;
-        throw Error(BISIM_GUARD, "superstep guard exceeded (" + std::to_string(hc.guard_count) + " > " +
+        throw Error(BISIM_GUARD, "superstep guard exceeded (" + std::to_string(ls.guard_count) + " > " +
                                      std::to_string(guard) + ")");
     }
 
     // ---- results
-    CK(cudaMemsetAsync(&ctrl->count, 0, 4, st));
-    k_count_leaders<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, block, ctrl);
+    CK(cudaMemsetAsync(leaders, 0, 4, st));
+    k_count_leaders<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, block, leaders);
     ++c.launches;
     if (j.block_out_on_device)
         CK(cudaMemcpyAsync(j.block_out, block, (int64_t)n * 4, cudaMemcpyDeviceToDevice, st));
     else
         CK(cudaMemcpyAsync(j.block_out, block, (int64_t)n * 4, cudaMemcpyDeviceToHost, st));
-    const int64_t R = hc.round;
+    const int64_t R = ls.round;
     const int64_t ncopy = std::min<int64_t>(std::min<int64_t>(R, j.splits_cap), splits_dev_cap);
     if (j.splits_out && ncopy > 0)
         CK(cudaMemcpyAsync(j.splits_out, splits, ncopy * 4, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&hc, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&h_leaders, leaders, 4, cudaMemcpyDeviceToHost, st));
     CK(cudaEventRecord(c.ev[5], st));
     CK(cudaStreamSynchronize(st));
-    S.final_blocks = hc.count;
+    S.final_blocks = h_leaders;
     S.t_h2d_ms = elapsed(c.ev[0], c.ev[1]);
     S.t_pre_ms = elapsed(c.ev[1], c.ev[2]);
     S.t_label_ms = elapsed(c.ev[2], c.ev[3]);
     S.t_alg_ms = elapsed(c.ev[3], c.ev[4]);
     S.t_d2h_ms = elapsed(c.ev[4], c.ev[5]);
-    // Algorithmic bytes of the loop: per round the
-    // dense state scans (block twice, slot offsets, leader offsets, mark
-    // words, unstable bitmap) plus per in-edge of C a slot read and a mark
-    // word set and clear, plus per split state block/new-leader traffic.
-    const int64_t per_round = j.bcrp ? (int64_t)n * (4 + 4 + 4 + 4 + 4) + (int64_t)L32 / 8 * 2 + nwords * 4
-                                     : (int64_t)n * (4 + 4) + nwords * 4 * 3;
-    S.bytes_alg = (R + 1) * per_round + (int64_t)hc.work_edges * (4 + 4 + 4 + 4) +
-                  (int64_t)hc.work_splits * (4 + 4 + 8 + 4 + 8);
+    S.bytes_alg = loop_bytes(j.bcrp, dense, n, L32, R, ls);
+    if (!dense && sp.trace) {
+        std::vector<unsigned long long> t(sp.trace_rounds * 8);
+        CK(cudaMemcpy(t.data(), sp.trace, t.size() * 8, cudaMemcpyDeviceToHost));
+        const char* path = getenv("BISIM_TRACE_FILE");
+        if (FILE* f = fopen(path ? path : "bisim_trace.csv", "w")) {
+            fprintf(f, "round,phaseA_ns,barrierA_ns,phaseB_ns,csize,w0_edges_cum,n_small,big_chunks,n_big\n");
+            for (int64_t r = 0; r < std::min<int64_t>(sp.trace_rounds, R); ++r) {
+                const unsigned long long* q = &t[r * 8];
+                fprintf(f, "%lld,%llu,%llu,%llu,%llu,%llu,%llu,%llu,%llu\n", (long long)r, q[1] - q[0], q[2] - q[1],
+                        q[3] - q[2], q[4], q[5], q[6], q[7] & 0xffffffffull, q[7] >> 32);
+            }
+            fclose(f);
+        }
+    }
     S.kernel_launches = c.launches;
     *j.st = S;
     return BISIM_OK;

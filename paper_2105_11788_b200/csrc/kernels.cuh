@@ -304,13 +304,13 @@ __global__ void k_scan_apply(int32_t* d, int64_t N, const int64_t* __restrict__ 
 // ---------------------------------------------------------------------------
 // Partition bookkeeping
 // ---------------------------------------------------------------------------
-__global__ void k_count_leaders(int32_t n, const int32_t* __restrict__ block, Ctrl* ctrl) {
+__global__ void k_count_leaders(int32_t n, const int32_t* __restrict__ block, int32_t* count) {
     int32_t c = 0;
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n;
          s += (int64_t)gridDim.x * blockDim.x)
         c += block[s] == s;
     c = __reduce_add_sync(kFull, c);
-    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&ctrl->count, c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
 }
 
 // unstable[leader] := true for every initial block (bcrp.py:226-229, rcpp.py:68-70)

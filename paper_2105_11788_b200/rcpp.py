@@ -86,7 +86,7 @@ def rcpp_arrays(n: int, src, dst, pi0, *, max_supersteps: int | None = None, obs
     splits = np.zeros(cap, np.int32)
     st = N.Stats()
     bridge = _ObserverBridge(observer) if observer is not None else None
-    opt = _options(device, N.MODE_STEPPED if observer is not None else mode, bridge)
+    opt = _options(device, mode, bridge)  # an observer implies stepped rounds
     rc = N.lib().bisim_rcpp_ex(n, src.size, N.ptr(src), N.ptr(dst), N.ptr(pi0), guard,
                                N.ptr(block), N.ptr(splits), cap, ctypes.byref(st),
                                ctypes.byref(opt))

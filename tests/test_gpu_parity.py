@@ -13,11 +13,28 @@ import pytest
 
 import _golden as G
 from oracle import oracle
-from paper_2105_11788_b200 import bcrp_arrays, rcpp_arrays
+import functools
+
+from paper_2105_11788_b200 import _native as N
+from paper_2105_11788_b200 import bcrp_arrays as _bcrp_arrays
+from paper_2105_11788_b200 import rcpp_arrays as _rcpp_arrays
 from paper_2105_11788_b200 import workloads as W
 from paper_2105_11788_b200.policy import SuperstepLimitError
 
 pytestmark = pytest.mark.gpu
+
+MODES = {"sparse": N.MODE_AUTO, "dense": N.MODE_DENSE}
+bcrp_arrays = rcpp_arrays = None  # bound per test by the `mode` fixture
+
+
+@pytest.fixture(params=list(MODES), autouse=True)
+def mode(request):
+    """Every parity test runs against both refinement loops."""
+    global bcrp_arrays, rcpp_arrays
+    m = MODES[request.param]
+    bcrp_arrays = functools.partial(_bcrp_arrays, mode=m)
+    rcpp_arrays = functools.partial(_rcpp_arrays, mode=m)
+    yield request.param
 
 
 def _same(block, stats, exp, what):
