@@ -189,6 +189,23 @@ def run_reference(args):
     return 0
 
 
+def reduce_max(value: float, device=None) -> float:
+    """Max over ranks (identity without a process group); timing rule: the
+    job time is the slowest rank's device time."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return value
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_throughput(units_per_rank: int, steps: int, world: int, ms_max: float) -> float:
+    """Whole-job (n+m)/s: every rank refines its own LTS `steps` times."""
+    return units_per_rank * steps * world / (ms_max / 1e3)
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -265,12 +282,7 @@ def run_b200(args):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        ms = e0.elapsed_time(e1)
-        if world > 1:
-            t = torch.tensor([ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms, sts
+        return reduce_max(e0.elapsed_time(e1), dev), sts
 
     # warm-up + correctness check against the known coarsest partition
     first = None
@@ -297,9 +309,8 @@ def run_b200(args):
         raise SystemExit("bench: host-path result differs from the known coarsest partition")
 
     R = sts[0].supersteps
-    units = (n + m) * args.steps * world
-    value = units / (ms / 1e3)
-    e2e = units / (ms_e2e / 1e3)
+    value = job_throughput(n + m, args.steps, world, ms)
+    e2e = job_throughput(n + m, args.steps, world, ms_e2e)
     t_alg = statistics.mean(s.t_alg_ms for s in sts)
     bytes_alg = statistics.mean(s.bytes_alg for s in sts)
     peak, peak_kind = measured_peak_hbm()
@@ -340,7 +351,7 @@ def run_b200(args):
                     "d2h_bytes_per_step": int(4 * n + 4 * R)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_refine (persistent refinement loop)",
+                         "kernel": "k_refine_sparse (persistent refinement loop)",
                          "peak_source": peak_kind,
                          "bytes_per_launch": bytes_alg, "launch_ms": t_alg},
             "cpu_baseline": cpu,
