@@ -21,6 +21,7 @@
 #include "../../include/bisim.h"
 #include "kernels.cuh"
 #include "kernels_sparse.cuh"
+#include "kernels_label.cuh"
 
 namespace bisim {
 namespace {
@@ -68,7 +69,8 @@ struct Ctx {
     std::mutex mu;
     DevBuf src, act, dst, pi0, lmask, off, rev_ptr, cursor, rev_slot, block, nl, mark, unstable,
         split_list, cmem, splits, ctrl, scan_tmp, rev2, members, bstart, bsize, touched, tblock,
-        small_list, big_list, big_base, tmp, scnt, smin, kcur, scur, counter, brange, bar, trace;
+        small_list, big_list, big_base, tmp, scnt, smin, kcur, scur, counter, brange, bar, trace, lhash, lkeys,
+        lmins;
     int launches = 0;
 };
 
@@ -319,7 +321,30 @@ int run(Job& j) {
     unsigned long long* nl = (unsigned long long*)c.nl.ensure((int64_t)n * 8);
     if (j.bcrp) {
         CK(cudaMemsetAsync(block, 0, (int64_t)n * 4, st));
-        if (A > 0) {
+        bool literal = A > 0 && getenv("BISIM_LITERAL_LABEL_ROUNDS") != nullptr;
+        if (A > 0 && !literal) {
+            // canonical grouping by label set (kernels_label.cuh), verified
+            uint64_t T = 1024;
+            while (T < 2ull * (uint64_t)n) T <<= 1;
+            auto* h = (unsigned long long*)c.lhash.ensure((int64_t)n * 8);
+            auto* keys = (unsigned long long*)c.lkeys.ensure(T * 8);
+            auto* mins = (int32_t*)c.lmins.ensure(T * 4 + 4);
+            int32_t* mismatch = mins + T;
+            CK(cudaMemsetAsync(keys, 0, T * 8, st));
+            CK(cudaMemsetAsync(mins, 0x7f, T * 4 + 4, st));
+            CK(cudaMemsetAsync(mismatch, 0, 4, st));
+            k_label_hash<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, W, lmask, h);
+            k_label_insert<<<c.sms * 2, 512, 0, st>>>(n, h, keys, mins, T - 1);
+            k_label_assign<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, W, h, keys, mins, T - 1, lmask, block,
+                                                                  mismatch);
+            c.launches += 3;
+            int32_t hm = 0;
+            CK(cudaMemcpyAsync(&hm, mismatch, 4, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            literal = hm != 0;  // a 64-bit hash collision: redo with the literal rounds
+            if (literal) CK(cudaMemsetAsync(block, 0, (int64_t)n * 4, st));
+        }
+        if (literal) {
             CK(cudaMemsetAsync(nl, 0, (int64_t)n * 8, st));
             int32_t nn = n, AA = A;
             const unsigned long long* lm = lmask;

@@ -290,3 +290,19 @@ def test_c5_vlts_lifted_truth():
     block, st, ns = bcrp_arrays(inst.n, inst.src, inst.act, inst.dst, inst.num_actions)
     assert np.array_equal(block, inst.truth)
     assert st.final_block_count == len(np.unique(inst.truth))
+
+
+def test_label_grouping_equals_literal_rounds(monkeypatch):
+    """The hash-grouped label pre-partition equals the literal |Act| rounds
+    of bcrp.py:144-184 (BISIM_LITERAL_LABEL_ROUNDS forces the latter)."""
+    for seed, (n, m, A) in enumerate([(3000, 9000, 5), (2000, 20000, 70), (5000, 5000, 200)]):
+        g = np.random.default_rng(100 + seed)
+        src = g.integers(0, n, m, dtype=np.int32)
+        act = g.integers(0, A, m, dtype=np.int32)
+        dst = g.integers(0, n, m, dtype=np.int32)
+        b1, s1, _ = bcrp_arrays(n, src, act, dst, A)
+        monkeypatch.setenv("BISIM_LITERAL_LABEL_ROUNDS", "1")
+        b2, s2, _ = bcrp_arrays(n, src, act, dst, A)
+        monkeypatch.delenv("BISIM_LITERAL_LABEL_ROUNDS")
+        assert np.array_equal(b1, b2) and s1 == s2
+        assert np.array_equal(b1, oracle.bcrp(n, src, act, dst, A, threads=4).block)
