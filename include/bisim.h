@@ -74,6 +74,7 @@ typedef struct bisim_stats {
     int64_t bytes_alg;       /* algorithmic bytes of the main loop */
     int32_t kernel_launches; /* kernels this call launched */
     int32_t mode;            /* BISIM_MODE_* actually used */
+    int64_t rounds_retired;  /* no-op rounds retired in bulk (counted in supersteps) */
 } bisim_stats;
 
 /* observer(iteration, block, n, user): called after every counted round in

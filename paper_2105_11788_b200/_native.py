@@ -37,7 +37,8 @@ class Stats(ctypes.Structure):
                 ("t_d2h_ms", ctypes.c_double),
                 ("bytes_alg", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int32),
-                ("mode", ctypes.c_int32)]
+                ("mode", ctypes.c_int32),
+                ("rounds_retired", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -159,7 +159,7 @@ struct LoopStatus {
     int64_t round = 0;
     int32_t done = 0, error = 0;
     int64_t guard_count = 0;
-    unsigned long long work_edges = 0, work_members = 0, work_splits = 0;
+    unsigned long long work_edges = 0, work_members = 0, work_splits = 0, retired = 0;
 };
 
 // Algorithmic bytes of the refinement loop ("Roofline"): the
@@ -453,6 +453,8 @@ int run(Job& j) {
         sp.splits = splits;
         sp.ctrl = (SCtrl*)ctrl;
         sp.bar = (GridBarrier*)c.bar.ensure(sizeof(GridBarrier));
+        // BISIM_NO_SKIP=1 disables no-op-round retirement (every round runs)
+        sp.allow_skip = getenv("BISIM_NO_SKIP") == nullptr ? 1 : 0;
         // developer tracing: BISIM_TRACE=<rounds> BISIM_TRACE_FILE=<path>
         if (const char* tr = getenv("BISIM_TRACE")) {
             sp.trace_rounds = atoll(tr);
@@ -492,7 +494,7 @@ int run(Job& j) {
             CK(cudaMemcpyAsync(&h, ctrl, sizeof(SCtrl), cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
             ls.round = h.round; ls.done = h.done; ls.error = h.error; ls.guard_count = h.guard_count;
-            ls.work_edges = h.work_edges; ls.work_members = h.work_members;
+            ls.work_edges = h.work_edges; ls.work_members = h.work_members; ls.retired = h.skipped_rounds;
         }
         return ls;
     };
@@ -575,6 +577,7 @@ int run(Job& j) {
         }
     }
     S.kernel_launches = c.launches;
+    S.rounds_retired = (int64_t)ls.retired;
     *j.st = S;
     return BISIM_OK;
 }

@@ -72,7 +72,16 @@ struct SCtrl {
     unsigned long long big_pack[2];     // (#big touched blocks << 32) | #chunks
     unsigned long long work_edges;      // sum of in(C)
     unsigned long long work_members;    // sum of touched-block sizes
+    int32_t heavy[2];                   // round touched a block of > 1 member
+    int32_t nontriv[2];                 // skip step: least non-trivial candidate
+    int32_t skipcnt[2];                 // skip step: rounds retired
+    int32_t skip_next[2];               // skip step: splitter after the window
+    unsigned long long skipped_rounds;  // statistics
 };
+
+// Window of unstable labels examined by one skip step (see k_refine_sparse).
+constexpr int32_t kSkipSpan = 32768;
+constexpr int32_t kSkipMaxEdges = 256;
 
 struct SparseParams {
     int32_t n;
@@ -110,6 +119,8 @@ struct SparseParams {
     GridBarrier* bar;
     unsigned long long* trace;  // optional: 4 globaltimer stamps per round (CTA 0)
     int64_t trace_rounds;
+    int32_t allow_skip;         // retire runs of no-op rounds in one step
+    int32_t pad2;
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -206,6 +217,7 @@ __device__ int32_t u_next_warp(const SparseParams& p, int32_t from) {
 __device__ __forceinline__ void register_block(const SparseParams& p, int cur, int32_t b) {
     SCtrl* ctl = p.ctrl;
     const int2 r = p.brange[b];
+    if (r.y > 1) ctl->heavy[cur] = 1;
     if (r.y <= 32) {
         const int32_t k = atomicAdd(&ctl->n_small[cur], 1);
         p.small_list[k] = make_int4(b, r.x, r.y, 0);
@@ -440,6 +452,39 @@ __device__ void big_split(const SparseParams& p, int cur, int64_t round, int32_t
     if (i == 0) atomicAnd(&p.tblock[l >> 5], ~(1u << (l & 31)));
 }
 
+// ---- no-op rounds ------------------------------------------------------------
+
+// Is the round whose splitter is c a no-op?  True when every in-edge source
+// of c's members lies in a singleton block: singletons never split (a leader
+// compares with itself), so the round changes nothing but unstable[c] --
+// no split, no raised label, no BCRP re-raise (bcrp.py:267-283).  Answers
+// false (the round then runs normally) for splitters of more than 32
+// members or more than kSkipMaxEdges in-edges.
+template <bool IDENT>
+__device__ __forceinline__ bool round_is_trivial(const SparseParams& p, int32_t c) {
+    const int2 r = p.brange[c];
+    if (r.y > 32) return false;
+    int32_t budget = kSkipMaxEdges;
+    for (int32_t i = 0; i < r.y; ++i) {
+        const int32_t t = p.members[r.x + i];
+        const int32_t e0 = p.rev_ptr[t], e1 = p.rev_ptr[t + 1];
+        if (e1 - e0 > budget) return false;
+        budget -= e1 - e0;
+        for (int32_t e = e0; e < e1; e += 4) {
+            int32_t s[4], b[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) s[k] = e + k < e1 ? (IDENT ? p.rev_src[e + k] : p.rev[e + k].y) : -1;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) b[k] = s[k] >= 0 ? p.block[s[k]] : -1;
+            bool single = true;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) single &= b[k] < 0 || p.brange[b[k]].y == 1;
+            if (!single) return false;
+        }
+    }
+    return true;
+}
+
 // ---- the persistent kernel ---------------------------------------------------
 
 template <bool IDENT>
@@ -458,10 +503,20 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
         const int32_t c = u_next_warp(p, 0);
         if (lane == 0) ctl->C0 = c;
     }
+    if (gtid == 0) {
+        ctl->nontriv[0] = ctl->nontriv[1] = kBig;
+        ctl->skipcnt[0] = ctl->skipcnt[1] = 0;
+    }
     grid_barrier(p.bar, gen);
     int32_t C = ld_vol(&ctl->C0);
     int64_t round = ld_vol(&ctl->round);
     unsigned long long my_edges = 0, my_members = 0;
+    // no-op-round retirement (only in persistent mode: an observer must see
+    // every round): tried after a round that touched singleton blocks only,
+    // with exponential back-off when a try retires nothing
+    bool try_skip = false;
+    int32_t cooldown = 0, backoff = 16;
+    int64_t skips = 0;
 
     for (int64_t done_here = 0;; ++done_here) {
         if (done_here == p.round_limit) break;
@@ -477,6 +532,63 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
             if (gtid == 0) ctl->done = 1;
             break;
         }
+
+        // ---- skip step: retire the maximal run of no-op rounds -------------
+        // The next rounds' splitters are the unstable labels in increasing
+        // order; a no-op round only removes its splitter from the unstable
+        // set, so every unstable label below the first non-trivial one in
+        // the window [C, C + kSkipSpan) is retired at once (0 splits each).
+        if (try_skip && p.round_limit == INT64_MAX &&
+            (!p.has_guard || (int64_t)p.A + round + kSkipSpan + 1 <= p.max_supersteps)) {
+            const int sp = (int)(skips & 1);
+            const int32_t lim = (int64_t)C + kSkipSpan < (int64_t)p.n ? C + kSkipSpan : p.n;
+            for (int32_t w = (C >> 5) + gwarp; w <= ((lim - 1) >> 5); w += nwarps) {
+                const int32_t c = (w << 5) + lane;
+                const bool cand = c >= C && c < lim && ((ld_vol(&p.U0[w]) >> lane) & 1u);
+                if (cand && !round_is_trivial<IDENT>(p, c)) atomicMin(&ctl->nontriv[sp], c);
+            }
+            grid_barrier(p.bar, gen);
+            const int32_t nt = ld_vol(&ctl->nontriv[sp]);
+            const int32_t end = min(nt, lim);
+            int32_t cnt = 0;
+            if (end > C) {
+                const int32_t wlast = (end - 1) >> 5;
+                for (int64_t w = (C >> 5) + gtid; w <= wlast; w += (int64_t)gridDim.x * blockDim.x) {
+                    uint32_t v = ld_vol(&p.U0[w]);
+                    if (w == (C >> 5)) v &= ~0u << (C & 31);
+                    if (w == wlast && (end & 31)) v &= (1u << (end & 31)) - 1u;
+                    if (v) {
+                        atomicAnd(&p.U0[w], ~v);
+                        cnt += __popc(v);
+                    }
+                }
+            }
+            cnt = __reduce_add_sync(kFull, cnt);
+            if (lane == 0 && cnt) atomicAdd(&ctl->skipcnt[sp], cnt);
+            if (gwarp == aux_warp) {
+                const int32_t nx = nt < lim ? nt : u_next_warp(p, lim);
+                if (lane == 0) {
+                    ctl->skip_next[sp] = nx;
+                    ctl->nontriv[sp ^ 1] = kBig;
+                    ctl->skipcnt[sp ^ 1] = 0;
+                }
+            }
+            grid_barrier(p.bar, gen);
+            const int32_t retired = ld_vol(&ctl->skipcnt[sp]);
+            round += retired;
+            C = ld_vol(&ctl->skip_next[sp]);
+            ++skips;
+            if (gtid == 0) ctl->skipped_rounds += (unsigned long long)retired;
+            if (retired == 0) {
+                try_skip = false;
+                cooldown = backoff;
+                backoff = min(backoff * 2, 4096);
+            } else {
+                backoff = 16;
+            }
+            continue;
+        }
+
         const int cur = (int)(round & 1), nxt = cur ^ 1;
         const bool tr = p.trace != nullptr && gtid == 0 && round < p.trace_rounds;
         if (tr) p.trace[round * 8 + 0] = globaltimer();
@@ -563,6 +675,7 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
         if (gtid == 0) {
             ctl->n_small[nxt] = 0;
             ctl->big_pack[nxt] = 0ull;
+            ctl->heavy[nxt] = 0;
         }
         const int32_t nsm = ld_vol(&ctl->n_small[cur]);
         const unsigned long long bp = ld_vol(&ctl->big_pack[cur]);
@@ -581,6 +694,8 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
         if (tr) p.trace[round * 8 + 3] = globaltimer();
         C = min(ld_vol(&ctl->next_min[cur]), ld_vol(&ctl->succ[cur]));
         ++round;
+        if (cooldown > 0) --cooldown;
+        try_skip = p.allow_skip && cooldown == 0 && ld_vol(&ctl->heavy[cur]) == 0;
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {

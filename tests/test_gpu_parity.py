@@ -306,3 +306,21 @@ def test_label_grouping_equals_literal_rounds(monkeypatch):
         monkeypatch.delenv("BISIM_LITERAL_LABEL_ROUNDS")
         assert np.array_equal(b1, b2) and s1 == s2
         assert np.array_equal(b1, oracle.bcrp(n, src, act, dst, A, threads=4).block)
+
+
+def test_noop_round_retirement_is_exact(monkeypatch):
+    """Retiring runs of no-op rounds (splitters whose in-edge sources all sit
+    in singleton blocks) gives the same RunStats as running every round."""
+    cases = [W.chain(3000), W.c2_kripke(n=20000, out_degree=3, seed=5),
+             W.c4_uniform(n=20000, m=60000, num_actions=40, seed=6)]
+    for inst in cases:
+        if inst.kind == "bcrp":
+            run = lambda: bcrp_arrays(inst.n, inst.src, inst.act, inst.dst, inst.num_actions)
+        else:
+            run = lambda: rcpp_arrays(inst.n, inst.src, inst.dst, inst.pi0)
+        b1, s1, n1 = run()
+        monkeypatch.setenv("BISIM_NO_SKIP", "1")
+        b2, s2, _ = run()
+        monkeypatch.delenv("BISIM_NO_SKIP")
+        assert np.array_equal(b1, b2), inst.name
+        assert s1 == s2, inst.name
