@@ -70,7 +70,7 @@ struct Ctx {
     DevBuf src, act, dst, pi0, lmask, off, rev_ptr, cursor, rev_slot, block, nl, mark, unstable,
         split_list, cmem, splits, ctrl, scan_tmp, rev2, members, bstart, bsize, touched, tblock,
         small_list, big_list, big_base, tmp, scnt, smin, kcur, scur, counter, brange, bar, trace, lhash, lkeys,
-        lmins;
+        lmins, sarr;
     int launches = 0;
 };
 
@@ -450,6 +450,7 @@ int run(Job& j) {
         sp.smin = (int32_t*)c.smin.ensure((int64_t)n * 4);
         sp.kcur = (int32_t*)c.kcur.ensure((int64_t)n * 4);
         sp.scur = (int32_t*)c.scur.ensure((int64_t)n * 4);
+        sp.sarr = (int32_t*)c.sarr.ensure((int64_t)n * 4);
         sp.splits = splits;
         sp.ctrl = (SCtrl*)ctrl;
         sp.bar = (GridBarrier*)c.bar.ensure(sizeof(GridBarrier));

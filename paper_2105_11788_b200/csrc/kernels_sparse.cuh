@@ -114,6 +114,7 @@ struct SparseParams {
     int32_t* smin;
     int32_t* kcur;
     int32_t* scur;
+    int32_t* sarr;        // per label: chunks of the block that have tagged (one-pass split)
     int32_t* splits;
     SCtrl* ctrl;
     GridBarrier* bar;
@@ -232,6 +233,7 @@ __device__ __forceinline__ void register_block(const SparseParams& p, int cur, i
         p.smin[b] = kBig;
         p.kcur[b] = 0;
         p.scur[b] = 0;
+        p.sarr[b] = 0;
     }
 }
 
@@ -450,6 +452,72 @@ __device__ void big_split(const SparseParams& p, int cur, int64_t round, int32_t
         clear_member<IDENT>(p, u, tu, ou, nr);
     }
     if (i == 0) atomicAnd(&p.tblock[l >> 5], ~(1u << (l & 31)));
+}
+
+// One-pass split of a big block's chunk, used when every phase-B work item
+// has its own warp (all items run concurrently, so waiting for the other
+// chunks of the block cannot deadlock).  The block's chunks publish their
+// split counts / minimum, bump an arrival counter, and wait for the last
+// one instead of a grid-wide barrier; compaction and clearing then follow
+// from registers.
+template <bool IDENT>
+__device__ int32_t big_onepass(const SparseParams& p, int cur, int64_t round, int32_t C, int32_t nbig,
+                               int32_t ci) {
+    const int lane = threadIdx.x & 31;
+    const int4 e = p.big_list[find_owner(p, nbig, ci)];
+    const int32_t l = e.x, bs = e.y, bz = e.z;
+    const int32_t i = ((ci - e.w) << 5) + lane;
+    const bool valid = i < bz;
+    const int32_t u = valid ? p.members[bs + i] : -1;
+    const bool tl = IDENT ? get_bit(p.mark, l) : get_bit(p.touched, l);
+    bool tu = false;
+    int32_t ou = 0, nr = 0;
+    const bool sp = valid && member_splits<IDENT>(p, u, l, tl, tu, ou, nr);
+    const unsigned bal = __ballot_sync(kFull, sp);
+    const int32_t wl = __reduce_min_sync(kFull, sp ? u : kBig);
+    const int32_t nch_b = (bz + 31) >> 5;
+    int32_t ns = 0, w = kBig;
+    if (lane == 0) {
+        if (bal) {
+            atomicAdd(&p.scnt[l], __popc(bal));
+            atomicMin(&p.smin[l], wl);
+        }
+        __threadfence();
+        atomicAdd(&p.sarr[l], 1);
+        while (ld_acquire_u32((const unsigned*)&p.sarr[l]) < (unsigned)nch_b) {
+        }
+        ns = ld_vol(&p.scnt[l]);
+        w = ld_vol(&p.smin[l]);
+    }
+    ns = __shfl_sync(kFull, ns, 0);
+    w = __shfl_sync(kFull, w, 0);
+    if (ns) {
+        const int32_t keep = bz - ns;
+        const unsigned kb = __ballot_sync(kFull, valid && !sp);
+        const unsigned lt = lanemask_lt();
+        int32_t sbase = 0, kbase = 0;
+        if (lane == 0) {
+            if (bal) sbase = atomicAdd(&p.scur[l], __popc(bal));
+            if (kb) kbase = atomicAdd(&p.kcur[l], __popc(kb));
+        }
+        sbase = __shfl_sync(kFull, sbase, 0);
+        kbase = __shfl_sync(kFull, kbase, 0);
+        if (valid) {
+            const int32_t np = sp ? bs + keep + sbase + __popc(bal & lt) : bs + kbase + __popc(kb & lt);
+            p.members[np] = u;
+            if (sp) p.block[u] = w;
+        }
+        if (i == 0) {
+            p.brange[l] = make_int2(bs, keep);
+            p.brange[w] = make_int2(bs + keep, ns);
+            raise_split(p, cur, round, l, w, C);
+        }
+    }
+    // every chunk has read the leader's marks before anyone clears: the
+    // arrival counter above is complete
+    if (valid) clear_member<IDENT>(p, u, tu, ou, nr);
+    if (i == 0) atomicAnd(&p.tblock[l >> 5], ~(1u << (l & 31)));
+    return min(32, bz - ((ci - e.w) << 5));
 }
 
 // ---- no-op rounds ------------------------------------------------------------
@@ -680,12 +748,14 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
         const int32_t nsm = ld_vol(&ctl->n_small[cur]);
         const unsigned long long bp = ld_vol(&ctl->big_pack[cur]);
         const int32_t nbig = (int32_t)(bp >> 32), nch = (int32_t)(bp & 0xffffffffu);
+        const bool one_pass = nsm + nch <= nwarps;  // every item on its own warp
         for (int32_t it = gwarp; it < nsm + nch; it += nwarps) {
             const int32_t cnt = it < nsm ? process_small<IDENT>(p, cur, round, C, p.small_list[it])
-                                         : big_tag<IDENT>(p, nbig, it - nsm);
+                                : one_pass ? big_onepass<IDENT>(p, cur, round, C, nbig, it - nsm)
+                                           : big_tag<IDENT>(p, nbig, it - nsm);
             if (lane == 0) my_members += (unsigned long long)cnt;
         }
-        if (nbig) {
+        if (nbig && !one_pass) {
             grid_barrier(p.bar, gen);
             for (int32_t it = gwarp; it < nch; it += nwarps) big_split<IDENT>(p, cur, round, C, nbig, it);
         }
