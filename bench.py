@@ -38,7 +38,8 @@ UNIT = "(n+m)/s"
 # Round counts of the default-seed workloads, measured by the GPU path and
 # pinned by tests/test_bench_contract.py; the CPU reference arm extrapolates
 # its sampled per-round time with them.
-KNOWN_SUPERSTEPS = {}
+KNOWN_SUPERSTEPS = {"c5": 6113, "c1": 13962, "c2": 1201621, "c3": 399998, "c4u": 5006404,
+                    "c4l": 24344}
 
 
 def make_instance(config: str, rank: int):
@@ -206,6 +207,24 @@ def job_throughput(units_per_rank: int, steps: int, world: int, ms_max: float) -
     return units_per_rank * steps * world / (ms_max / 1e3)
 
 
+def empty_round_floor_us(device: int, n: int = 20000) -> float:
+    """Latency floor of one refinement round: RCPP on an edge-free system
+    with a discrete pi0 runs n rounds whose splitter has no in-edge (pure
+    control + barriers); no-op retirement disabled so every round runs."""
+    from paper_2105_11788_b200 import rcpp_arrays
+    old = os.environ.get("BISIM_NO_SKIP")
+    os.environ["BISIM_NO_SKIP"] = "1"
+    try:
+        empty = np.zeros(0, np.int32)
+        _, st, ns = rcpp_arrays(n, empty, empty, np.arange(n, dtype=np.int32), device=device)
+    finally:
+        if old is None:
+            del os.environ["BISIM_NO_SKIP"]
+        else:
+            os.environ["BISIM_NO_SKIP"] = old
+    return ns["t_alg_ms"] * 1e3 / max(st.supersteps, 1)
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -308,6 +327,8 @@ def run_b200(args):
     if inst.truth is not None and not np.array_equal(h_block, inst.truth):
         raise SystemExit("bench: host-path result differs from the known coarsest partition")
 
+    floor_us = empty_round_floor_us(local) if rank == 0 else None
+
     R = sts[0].supersteps
     value = job_throughput(n + m, args.steps, world, ms)
     e2e = job_throughput(n + m, args.steps, world, ms_e2e)
@@ -345,6 +366,8 @@ def run_b200(args):
                          "label": statistics.mean(s.t_label_ms for s in sts),
                          "alg": t_alg},
             "per_round_us": t_alg * 1e3 / max(R, 1),
+            "per_round_floor_us": floor_us,
+            "rounds_retired": sts[0].rounds_retired,
             "e2e": {"value": e2e, "unit": UNIT, "ms_per_step": ms_e2e / args.steps,
                     "h2d_bytes_per_step": int(4 * m * (3 if inst.kind == "bcrp" else 2)
                                               + (4 * n if inst.kind == "rcpp" else 0)),
