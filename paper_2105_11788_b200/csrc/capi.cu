@@ -70,7 +70,7 @@ struct Ctx {
     DevBuf src, act, dst, pi0, lmask, off, rev_ptr, cursor, rev_slot, block, nl, mark, unstable,
         split_list, cmem, splits, ctrl, scan_tmp, rev2, members, bstart, bsize, touched, tblock,
         small_list, big_list, big_base, tmp, scnt, smin, kcur, scur, counter, brange, bar, trace, lhash, lkeys,
-        lmins, sarr;
+        lmins, sarr, big_list4, big_base4;
     int launches = 0;
 };
 
@@ -445,6 +445,8 @@ int run(Job& j) {
         sp.small_list = (int4*)c.small_list.ensure((int64_t)n * 16);
         sp.big_list = (int4*)c.big_list.ensure(((int64_t)n / 32 + 2) * 16);
         sp.big_base = (int32_t*)c.big_base.ensure(((int64_t)n / 32 + 2) * 4);
+        sp.big_list4 = (int4*)c.big_list4.ensure(((int64_t)n / 32 + 2) * 16);
+        sp.big_base4 = (int32_t*)c.big_base4.ensure(((int64_t)n / 32 + 2) * 4);
         sp.tmp = (int32_t*)c.tmp.ensure((int64_t)n * 4);
         sp.scnt = (int32_t*)c.scnt.ensure((int64_t)n * 4);
         sp.smin = (int32_t*)c.smin.ensure((int64_t)n * 4);

@@ -69,7 +69,8 @@ struct SCtrl {
     int32_t succ[2];                    // successor of C in unstable \ {C}
     int32_t n_small[2];                 // touched blocks of <= 32 members
     int32_t pad1[2];
-    unsigned long long big_pack[2];     // (#big touched blocks << 32) | #chunks
+    unsigned long long big_pack[2];     // (#big touched blocks << 32) | #32-member chunks
+    unsigned long long big_pack4[2];    // same for the 128-member chunk layout
     unsigned long long work_edges;      // sum of in(C)
     unsigned long long work_members;    // sum of touched-block sizes
     int32_t heavy[2];                   // round touched a block of > 1 member
@@ -82,6 +83,7 @@ struct SCtrl {
 // Window of unstable labels examined by one skip step (see k_refine_sparse).
 constexpr int32_t kSkipSpan = 32768;
 constexpr int32_t kSkipMaxEdges = 256;
+constexpr int kWide = 4;  // members per lane in the wide big-block chunk layout (kernels_big.cuh)
 
 struct SparseParams {
     int32_t n;
@@ -109,6 +111,8 @@ struct SparseParams {
     int4* small_list;     // touched blocks of <= 32 members: (label, start, size, -)
     int4* big_list;       // larger touched blocks: (label, start, size, first chunk)
     int32_t* big_base;    // first chunk of each big touched block (ascending)
+    int4* big_list4;      // the same blocks in the kWide chunk layout
+    int32_t* big_base4;
     int32_t* tmp;         // per member position: member, or -1-member if split
     int32_t* scnt;        // per label: split count / min split / compaction cursors
     int32_t* smin;
@@ -223,12 +227,19 @@ __device__ __forceinline__ void register_block(const SparseParams& p, int cur, i
         const int32_t k = atomicAdd(&ctl->n_small[cur], 1);
         p.small_list[k] = make_int4(b, r.x, r.y, 0);
     } else {
-        const int32_t nch = (r.y + 31) >> 5;
+        // two chunk layouts (kernels_big.cuh); each list is ordered by its
+        // own packed counter, so its first-chunk column ascends
+        const int32_t nch1 = (r.y + 31) >> 5, nch4 = (r.y + 32 * kWide - 1) / (32 * kWide);
         const unsigned long long pk =
-            atomicAdd(&ctl->big_pack[cur], (1ull << 32) | (unsigned long long)nch);
+            atomicAdd(&ctl->big_pack[cur], (1ull << 32) | (unsigned long long)nch1);
+        const unsigned long long pk4 =
+            atomicAdd(&ctl->big_pack4[cur], (1ull << 32) | (unsigned long long)nch4);
         const int32_t k = (int32_t)(pk >> 32), base = (int32_t)(pk & 0xffffffffu);
+        const int32_t k4 = (int32_t)(pk4 >> 32), base4 = (int32_t)(pk4 & 0xffffffffu);
         p.big_list[k] = make_int4(b, r.x, r.y, base);
         p.big_base[k] = base;
+        p.big_list4[k4] = make_int4(b, r.x, r.y, base4);
+        p.big_base4[k4] = base4;
         p.scnt[b] = 0;
         p.smin[b] = kBig;
         p.kcur[b] = 0;
@@ -356,169 +367,7 @@ __device__ int32_t process_small(const SparseParams& p, int cur, int64_t round, 
     return bz;
 }
 
-// Owner of chunk ci among the big touched blocks (bases ascending).
-__device__ __forceinline__ int32_t find_owner(const SparseParams& p, int32_t nbig, int32_t ci) {
-    const int lane = threadIdx.x & 31;
-    int32_t lo = 0, hi = nbig;
-    while (hi - lo > 32) {
-        const int32_t stride = (hi - lo + 31) >> 5;
-        const int32_t idx = lo + lane * stride;
-        const int32_t v = idx < hi ? p.big_base[idx] : 0x7fffffff;
-        const unsigned b = __ballot_sync(kFull, v <= ci);
-        const int32_t last = 31 - __clz(b);
-        lo = lo + last * stride;
-        hi = min(lo + stride, hi);
-    }
-    const int32_t idx = lo + lane;
-    const int32_t v = idx < hi ? p.big_base[idx] : 0x7fffffff;
-    const unsigned b = __ballot_sync(kFull, v <= ci);
-    return lo + 31 - __clz(b);
-}
-
-template <bool IDENT>
-__device__ int32_t big_tag(const SparseParams& p, int32_t nbig, int32_t ci) {
-    const int lane = threadIdx.x & 31;
-    const int4 e = p.big_list[find_owner(p, nbig, ci)];
-    const int32_t l = e.x, bs = e.y, bz = e.z;
-    const int32_t i = ((ci - e.w) << 5) + lane;
-    const bool valid = i < bz;
-    const int32_t u = valid ? p.members[bs + i] : -1;
-    const bool tl = IDENT ? get_bit(p.mark, l) : get_bit(p.touched, l);
-    bool tu = false;
-    int32_t ou = 0, nr = 0;
-    const bool sp = valid && member_splits<IDENT>(p, u, l, tl, tu, ou, nr);
-    if (valid) p.tmp[bs + i] = sp ? -1 - u : u;
-    const unsigned bal = __ballot_sync(kFull, sp);
-    if (bal) {
-        const int32_t w = __reduce_min_sync(kFull, sp ? u : kBig);
-        if (lane == 0) {
-            atomicAdd(&p.scnt[l], __popc(bal));
-            atomicMin(&p.smin[l], w);
-        }
-    }
-    return min(32, bz - ((ci - e.w) << 5));
-}
-
-template <bool IDENT>
-__device__ void big_split(const SparseParams& p, int cur, int64_t round, int32_t C, int32_t nbig,
-                          int32_t ci) {
-    const int lane = threadIdx.x & 31;
-    const int4 e = p.big_list[find_owner(p, nbig, ci)];
-    const int32_t l = e.x, bs = e.y, bz = e.z;
-    const int32_t i = ((ci - e.w) << 5) + lane;
-    const bool valid = i < bz;
-    const int32_t code = valid ? p.tmp[bs + i] : 0;
-    const bool sp = valid && code < 0;
-    const int32_t u = sp ? -1 - code : code;
-    const int32_t ns = p.scnt[l];
-    if (ns) {
-        const int32_t w = p.smin[l];
-        const int32_t keep = bz - ns;
-        const unsigned bal = __ballot_sync(kFull, sp);
-        const unsigned kb = __ballot_sync(kFull, valid && !sp);
-        const unsigned lt = lanemask_lt();
-        int32_t sbase = 0, kbase = 0;
-        if (lane == 0) {
-            if (bal) sbase = atomicAdd(&p.scur[l], __popc(bal));
-            if (kb) kbase = atomicAdd(&p.kcur[l], __popc(kb));
-        }
-        sbase = __shfl_sync(kFull, sbase, 0);
-        kbase = __shfl_sync(kFull, kbase, 0);
-        if (valid) {
-            const int32_t np = sp ? bs + keep + sbase + __popc(bal & lt) : bs + kbase + __popc(kb & lt);
-            p.members[np] = u;
-            if (sp) p.block[u] = w;
-        }
-        if (i == 0) {  // first chunk, lane 0
-            p.brange[l] = make_int2(bs, keep);
-            p.brange[w] = make_int2(bs + keep, ns);
-            raise_split(p, cur, round, l, w, C);
-        }
-    }
-    if (valid) {
-        bool tu;
-        int32_t ou = 0, nr = 0;
-        if (IDENT) {
-            tu = get_bit(p.mark, u);
-            ou = u;
-            nr = 1;
-        } else {
-            tu = get_bit(p.touched, u);
-            if (tu) {
-                ou = p.off[u];
-                nr = p.off[u + 1] - ou;
-            }
-        }
-        clear_member<IDENT>(p, u, tu, ou, nr);
-    }
-    if (i == 0) atomicAnd(&p.tblock[l >> 5], ~(1u << (l & 31)));
-}
-
-// One-pass split of a big block's chunk, used when every phase-B work item
-// has its own warp (all items run concurrently, so waiting for the other
-// chunks of the block cannot deadlock).  The block's chunks publish their
-// split counts / minimum, bump an arrival counter, and wait for the last
-// one instead of a grid-wide barrier; compaction and clearing then follow
-// from registers.
-template <bool IDENT>
-__device__ int32_t big_onepass(const SparseParams& p, int cur, int64_t round, int32_t C, int32_t nbig,
-                               int32_t ci) {
-    const int lane = threadIdx.x & 31;
-    const int4 e = p.big_list[find_owner(p, nbig, ci)];
-    const int32_t l = e.x, bs = e.y, bz = e.z;
-    const int32_t i = ((ci - e.w) << 5) + lane;
-    const bool valid = i < bz;
-    const int32_t u = valid ? p.members[bs + i] : -1;
-    const bool tl = IDENT ? get_bit(p.mark, l) : get_bit(p.touched, l);
-    bool tu = false;
-    int32_t ou = 0, nr = 0;
-    const bool sp = valid && member_splits<IDENT>(p, u, l, tl, tu, ou, nr);
-    const unsigned bal = __ballot_sync(kFull, sp);
-    const int32_t wl = __reduce_min_sync(kFull, sp ? u : kBig);
-    const int32_t nch_b = (bz + 31) >> 5;
-    int32_t ns = 0, w = kBig;
-    if (lane == 0) {
-        if (bal) {
-            atomicAdd(&p.scnt[l], __popc(bal));
-            atomicMin(&p.smin[l], wl);
-        }
-        __threadfence();
-        atomicAdd(&p.sarr[l], 1);
-        while (ld_acquire_u32((const unsigned*)&p.sarr[l]) < (unsigned)nch_b) {
-        }
-        ns = ld_vol(&p.scnt[l]);
-        w = ld_vol(&p.smin[l]);
-    }
-    ns = __shfl_sync(kFull, ns, 0);
-    w = __shfl_sync(kFull, w, 0);
-    if (ns) {
-        const int32_t keep = bz - ns;
-        const unsigned kb = __ballot_sync(kFull, valid && !sp);
-        const unsigned lt = lanemask_lt();
-        int32_t sbase = 0, kbase = 0;
-        if (lane == 0) {
-            if (bal) sbase = atomicAdd(&p.scur[l], __popc(bal));
-            if (kb) kbase = atomicAdd(&p.kcur[l], __popc(kb));
-        }
-        sbase = __shfl_sync(kFull, sbase, 0);
-        kbase = __shfl_sync(kFull, kbase, 0);
-        if (valid) {
-            const int32_t np = sp ? bs + keep + sbase + __popc(bal & lt) : bs + kbase + __popc(kb & lt);
-            p.members[np] = u;
-            if (sp) p.block[u] = w;
-        }
-        if (i == 0) {
-            p.brange[l] = make_int2(bs, keep);
-            p.brange[w] = make_int2(bs + keep, ns);
-            raise_split(p, cur, round, l, w, C);
-        }
-    }
-    // every chunk has read the leader's marks before anyone clears: the
-    // arrival counter above is complete
-    if (valid) clear_member<IDENT>(p, u, tu, ou, nr);
-    if (i == 0) atomicAnd(&p.tblock[l >> 5], ~(1u << (l & 31)));
-    return min(32, bz - ((ci - e.w) << 5));
-}
+#include "kernels_big.cuh"
 
 // ---- no-op rounds ------------------------------------------------------------
 
@@ -560,7 +409,9 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
     SCtrl* ctl = p.ctrl;
     const int lane = threadIdx.x & 31;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int32_t gwarp = (int32_t)(gtid >> 5);
+    // logical warp id, CTA-minor: consecutive work items land on different
+    // SMs, so a small round's work is spread over the whole chip
+    const int32_t gwarp = (int32_t)((threadIdx.x >> 5) * gridDim.x + blockIdx.x);
     const int32_t nwarps = (int32_t)(((int64_t)gridDim.x * blockDim.x) >> 5);
     const int32_t aux_warp = nwarps - 1;  // keeps the unstable-set bookkeeping off phase A's work
     unsigned gen = 0;
@@ -743,21 +594,28 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
         if (gtid == 0) {
             ctl->n_small[nxt] = 0;
             ctl->big_pack[nxt] = 0ull;
+            ctl->big_pack4[nxt] = 0ull;
             ctl->heavy[nxt] = 0;
         }
         const int32_t nsm = ld_vol(&ctl->n_small[cur]);
         const unsigned long long bp = ld_vol(&ctl->big_pack[cur]);
-        const int32_t nbig = (int32_t)(bp >> 32), nch = (int32_t)(bp & 0xffffffffu);
-        const bool one_pass = nsm + nch <= nwarps;  // every item on its own warp
+        const unsigned long long bp4 = ld_vol(&ctl->big_pack4[cur]);
+        const int32_t nbig = (int32_t)(bp >> 32), nch1 = (int32_t)(bp & 0xffffffffu);
+        const int32_t nch4 = (int32_t)(bp4 & 0xffffffffu);
+        // chunk layout and pass count for this round (kernels_big.cuh)
+        const int mode_b = nsm + nch1 <= nwarps ? 0 : (nsm + nch4 <= nwarps ? 1 : 2);
+        const int32_t nch = mode_b == 0 ? nch1 : nch4;
         for (int32_t it = gwarp; it < nsm + nch; it += nwarps) {
-            const int32_t cnt = it < nsm ? process_small<IDENT>(p, cur, round, C, p.small_list[it])
-                                : one_pass ? big_onepass<IDENT>(p, cur, round, C, nbig, it - nsm)
-                                           : big_tag<IDENT>(p, nbig, it - nsm);
+            int32_t cnt;
+            if (it < nsm) cnt = process_small<IDENT>(p, cur, round, C, p.small_list[it]);
+            else if (mode_b == 0) cnt = big_onepass<IDENT, 1>(p, cur, round, C, nbig, it - nsm);
+            else if (mode_b == 1) cnt = big_onepass<IDENT, kWide>(p, cur, round, C, nbig, it - nsm);
+            else cnt = big_tag<IDENT, kWide>(p, nbig, it - nsm);
             if (lane == 0) my_members += (unsigned long long)cnt;
         }
-        if (nbig && !one_pass) {
+        if (mode_b == 2) {
             grid_barrier(p.bar, gen);
-            for (int32_t it = gwarp; it < nch; it += nwarps) big_split<IDENT>(p, cur, round, C, nbig, it);
+            for (int32_t it = gwarp; it < nch; it += nwarps) big_split<IDENT, kWide>(p, cur, round, C, nbig, it);
         }
         for (int k = threadIdx.x; k < kSeen; k += blockDim.x) s_seen[k] = -1;
         grid_barrier(p.bar, gen);
