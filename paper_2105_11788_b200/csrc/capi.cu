@@ -458,6 +458,9 @@ int run(Job& j) {
         sp.bar = (GridBarrier*)c.bar.ensure(sizeof(GridBarrier));
         // BISIM_NO_SKIP=1 disables no-op-round retirement (every round runs)
         sp.allow_skip = getenv("BISIM_NO_SKIP") == nullptr ? 1 : 0;
+        sp.cta_minor = getenv("BISIM_CTA_MAJOR") == nullptr ? 1 : 0;
+        // BISIM_NO_SOLO=1 keeps every round on the whole grid
+        sp.allow_solo = getenv("BISIM_NO_SOLO") == nullptr ? 1 : 0;
         // developer tracing: BISIM_TRACE=<rounds> BISIM_TRACE_FILE=<path>
         if (const char* tr = getenv("BISIM_TRACE")) {
             sp.trace_rounds = atoll(tr);

@@ -1,0 +1,339 @@
+// kernels_loop.cuh -- the persistent refinement loop (default mode).
+//
+// Included inside namespace bisim by kernels_sparse.cuh.  One cooperative
+// launch runs every round (bcrp.py:286-308 / rcpp.py:240-252).  A round is
+// executed by a "team":
+//
+//   grid team  all 148 CTAs, grid barriers between phases (~1.3 us each);
+//   solo team  CTA 0 alone, __syncthreads between phases, while the other
+//              CTAs park on a hand-over counter.  Used for small rounds
+//              (splitter of <= kSoloMaxC members and a previous round with
+//              <= kSoloMaxItems phase-B work items), where the grid barrier
+//              round trips dominate.  CTA 0 hands the grid back as soon as a
+//              round looks bigger, or a skip step is due.
+//
+// Both teams run the same phase code; only the work distribution (warp ids,
+// warp count) and the phase barrier differ, so rounds are bit-identical.
+#pragma once
+
+constexpr int32_t kSoloMaxC = 64;
+constexpr int32_t kSoloMaxItems = 64;
+constexpr int32_t kSoloSkipSpan = 1024;  // skip-step window of the solo team
+
+template <bool IDENT>
+__global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParams p) {
+    SCtrl* ctl = p.ctrl;
+    const int lane = threadIdx.x & 31;
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
+    // logical warp id, CTA-minor: consecutive work items land on different
+    // SMs, so a small round's work is spread over the whole chip
+    const int32_t gwarp = p.cta_minor ? (int32_t)((threadIdx.x >> 5) * gridDim.x + blockIdx.x)
+                                      : (int32_t)(gtid >> 5);
+    const int32_t nwarps = (int32_t)(gsize >> 5);
+    unsigned gen = 0;
+    __shared__ int32_t s_seen[kSeen];
+    for (int k = threadIdx.x; k < kSeen; k += blockDim.x) s_seen[k] = -1;
+
+    if (gwarp == nwarps - 1) {
+        const int32_t c = u_next_warp(p, 0);
+        if (lane == 0) ctl->C0 = c;
+    }
+    if (gtid == 0) {
+        ctl->nontriv[0] = ctl->nontriv[1] = kBig;
+        ctl->skipcnt[0] = ctl->skipcnt[1] = 0;
+        ctl->items_last = kBig;
+    }
+    grid_barrier(p.bar, gen);
+    int32_t C = ld_vol(&ctl->C0);
+    int64_t round = ld_vol(&ctl->round);
+    unsigned long long my_edges = 0, my_members = 0;
+    // no-op-round retirement (only in persistent mode: an observer must see
+    // every round): tried after a round that touched singleton blocks only,
+    // with exponential back-off when a try retires nothing
+    bool try_skip = false;
+    int32_t cooldown = 0, backoff = 16;
+    int64_t skips = 0;
+    const bool solo_ok = p.allow_solo && p.round_limit == INT64_MAX && gridDim.x > 1;
+    bool solo = false;     // this CTA is in a solo stretch (CTA 0 working, others parked)
+    bool fresh = false;    // CTA 0: first solo round of a stretch
+    unsigned wakes = 0;    // hand-overs so far; identical on every CTA
+    unsigned stretches = 0;
+
+    for (int64_t done_here = 0;; ++done_here) {
+        // ---- parked CTAs: wait until CTA 0 hands the grid back or stops ----
+        if (solo && blockIdx.x != 0) {
+            if (threadIdx.x == 0) {
+                // acknowledge: this CTA has read everything the solo decision
+                // used, CTA 0 may now modify the partition
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&ctl->parked) : "memory");
+                while (ld_acquire_u32(&ctl->wake) == wakes) __nanosleep(64);
+            }
+            __syncthreads();
+            ++wakes;
+            solo = false;
+            if (ld_vol(&ctl->stop)) break;
+            C = ld_vol(&ctl->C0);
+            round = ld_vol(&ctl->round);
+            try_skip = ld_vol(&ctl->pub_try_skip) != 0;
+            cooldown = ld_vol(&ctl->pub_cooldown);
+            backoff = ld_vol(&ctl->pub_backoff);
+            skips = ld_vol(&ctl->pub_skips);
+        }
+        if (done_here == p.round_limit) break;
+        const int64_t steps = (int64_t)p.A + round + 1;
+        const bool guard_hit = p.has_guard && steps > p.max_supersteps;
+        if (guard_hit || C == kBig) {
+            if (gtid == 0) {
+                if (guard_hit) {
+                    ctl->error = 2;
+                    ctl->guard_count = steps;
+                } else {
+                    ctl->done = 1;
+                }
+                if (solo) {  // release the parked CTAs
+                    ctl->stop = 1;
+                    __threadfence();
+                    atomicAdd(&ctl->wake, 1u);
+                }
+            }
+            break;
+        }
+
+        // ---- CTA 0 in a solo stretch: keep going alone or hand back --------
+        if (solo) {
+            if (fresh) {  // wait until every other CTA has parked
+                if (threadIdx.x == 0) {
+                    const unsigned target = stretches * (gridDim.x - 1);
+                    while ((int)(ld_acquire_u32(&ctl->parked) - target) < 0) {
+                    }
+                }
+                __syncthreads();
+                fresh = false;
+            }
+            const bool stay = p.brange[C].y <= kSoloMaxC &&
+                              ld_vol(&ctl->items_last) <= kSoloMaxItems;
+            if (!stay) {
+                if (threadIdx.x == 0) {
+                    ctl->C0 = C;
+                    ctl->round = round;
+                    ctl->pub_try_skip = try_skip ? 1 : 0;
+                    ctl->pub_cooldown = cooldown;
+                    ctl->pub_backoff = backoff;
+                    ctl->pub_skips = skips;
+                    __threadfence();
+                    atomicAdd(&ctl->wake, 1u);
+                }
+                ++wakes;
+                solo = false;
+            }
+        }
+
+        // the team running this round
+        const int32_t tw = solo ? (int32_t)(threadIdx.x >> 5) : gwarp;
+        const int32_t tnw = solo ? (int32_t)(blockDim.x >> 5) : nwarps;
+        const int64_t ttid = solo ? (int64_t)threadIdx.x : gtid;
+        const int64_t tnt = solo ? (int64_t)blockDim.x : gsize;
+        const bool aux = tw == tnw - 1;  // unstable-set bookkeeping, off phase A's critical work
+
+        // ---- skip step: retire the maximal run of no-op rounds -------------
+        // The next rounds' splitters are the unstable labels in increasing
+        // order; a no-op round only removes its splitter from the unstable
+        // set, so every unstable label below the first non-trivial one in
+        // the window [C, C + span) is retired at once (0 splits each).  The
+        // solo team uses a 1024-label window (one U0 word per warp).
+        const int32_t span = solo ? kSoloSkipSpan : kSkipSpan;
+        if (try_skip && p.round_limit == INT64_MAX &&
+            (!p.has_guard || (int64_t)p.A + round + span + 1 <= p.max_supersteps)) {
+            const int sp = (int)(skips & 1);
+            const int32_t lim = (int64_t)C + span < (int64_t)p.n ? C + span : p.n;
+            for (int32_t w = (C >> 5) + tw; w <= ((lim - 1) >> 5); w += tnw) {
+                const int32_t c = (w << 5) + lane;
+                const bool cand = c >= C && c < lim && ((ld_vol(&p.U0[w]) >> lane) & 1u);
+                if (cand && !round_is_trivial<IDENT>(p, c)) atomicMin(&ctl->nontriv[sp], c);
+            }
+            if (solo) __syncthreads();
+            else grid_barrier(p.bar, gen);
+            const int32_t nt = ld_vol(&ctl->nontriv[sp]);
+            const int32_t end = min(nt, lim);
+            int32_t cnt = 0;
+            if (end > C) {
+                const int32_t wlast = (end - 1) >> 5;
+                for (int64_t w = (C >> 5) + ttid; w <= wlast; w += tnt) {
+                    uint32_t v = ld_vol(&p.U0[w]);
+                    if (w == (C >> 5)) v &= ~0u << (C & 31);
+                    if (w == wlast && (end & 31)) v &= (1u << (end & 31)) - 1u;
+                    if (v) {
+                        atomicAnd(&p.U0[w], ~v);
+                        cnt += __popc(v);
+                    }
+                }
+            }
+            cnt = __reduce_add_sync(kFull, cnt);
+            if (lane == 0 && cnt) atomicAdd(&ctl->skipcnt[sp], cnt);
+            if (aux) {
+                const int32_t nx = nt < lim ? nt : u_next_warp(p, lim);
+                if (lane == 0) {
+                    ctl->skip_next[sp] = nx;
+                    ctl->nontriv[sp ^ 1] = kBig;
+                    ctl->skipcnt[sp ^ 1] = 0;
+                }
+            }
+            if (solo) __syncthreads();
+            else grid_barrier(p.bar, gen);
+            const int32_t retired = ld_vol(&ctl->skipcnt[sp]);
+            round += retired;
+            C = ld_vol(&ctl->skip_next[sp]);
+            ++skips;
+            if (gtid == 0) ctl->skipped_rounds += (unsigned long long)retired;
+            if (retired == 0) {
+                try_skip = false;
+                cooldown = backoff;
+                backoff = min(backoff * 2, 4096);
+            } else {
+                backoff = 16;
+            }
+            continue;
+        }
+
+        const int cur = (int)(round & 1), nxt = cur ^ 1;
+        const bool tr = p.trace != nullptr && gtid == 0 && round < p.trace_rounds;
+        if (tr) p.trace[round * 8 + 0] = globaltimer();
+
+        // ---- phase A: mark the in-edges of C's members ----------------------
+        if (aux) {
+            u_clear_warp(p, C);
+            const int32_t sc = u_next_warp(p, C + 1);
+            if (lane == 0) {
+                ctl->succ[cur] = sc;
+                ctl->next_min[cur] = kBig;
+            }
+        }
+        {
+            const int2 cr = p.brange[C];
+            const int32_t cs = cr.x, cz = cr.y;
+            // members per warp: spread small splitters one member per warp so
+            // their in-edges are walked by as many warps as possible
+            const int32_t g = cz >= tnw * 32 ? 32 : max(1, (cz + tnw - 1) / tnw);
+            for (int64_t i0 = (int64_t)tw * g; i0 < cz; i0 += (int64_t)tnw * g) {
+                const int64_t i = i0 + lane;
+                int32_t e0 = 0, d = 0;
+                if (lane < g && i < cz) {
+                    const int32_t t = p.members[cs + i];
+                    e0 = p.rev_ptr[t];
+                    d = p.rev_ptr[t + 1] - e0;
+                }
+                int32_t incl = d;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int32_t y = __shfl_up_sync(kFull, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                const int32_t total = __shfl_sync(kFull, incl, 31);
+                const int32_t excl = incl - d;
+                my_edges += (unsigned long long)d;
+                for (int32_t k0 = 0; k0 < total; k0 += 32) {
+                    const int32_t k = k0 + lane;
+                    // owner lane j: the last lane with excl_j <= k
+                    int32_t j = 0;
+#pragma unroll
+                    for (int step = 16; step; step >>= 1) {
+                        const int32_t ex = __shfl_sync(kFull, excl, j + step);
+                        if (ex <= k) j += step;
+                    }
+                    const int32_t ej = __shfl_sync(kFull, e0, j);
+                    const int32_t xj = __shfl_sync(kFull, excl, j);
+                    const bool act = k < total;
+                    int32_t s = 0;
+                    if (act) {
+                        const int32_t e = ej + (k - xj);
+                        if (IDENT) {
+                            s = p.rev_src[e];
+                            atomicOr(&p.mark[s >> 5], 1u << (s & 31));
+                        } else {
+                            const int2 r = p.rev[e];
+                            s = r.y;
+                            atomicOr(&p.mark[r.x >> 5], 1u << (r.x & 31));
+                            atomicOr(&p.touched[s >> 5], 1u << (s & 31));
+                        }
+                    }
+                    const int32_t b = act ? p.block[s] : 0;
+                    const unsigned same = __match_any_sync(kFull, act ? b : -1 - lane);
+                    const bool rep = act && lane == __ffs(same) - 1;
+                    if (rep && cta_first(s_seen, b)) {
+                        const uint32_t bit = 1u << (b & 31);
+                        if (!(ld_vol(&p.tblock[b >> 5]) & bit) && !(atomicOr(&p.tblock[b >> 5], bit) & bit))
+                            register_block(p, cur, b);
+                    }
+                }
+            }
+        }
+        if (tr) p.trace[round * 8 + 1] = globaltimer();
+        if (solo) __syncthreads();
+        else grid_barrier(p.bar, gen);
+        if (tr) {
+            p.trace[round * 8 + 2] = globaltimer();
+            p.trace[round * 8 + 4] = p.brange[C].y;
+            p.trace[round * 8 + 5] = solo ? 1 : 0;
+            p.trace[round * 8 + 6] = ld_vol(&ctl->n_small[cur]);
+            p.trace[round * 8 + 7] = ld_vol(&ctl->big_pack[cur]);
+        }
+
+        // ---- phase B: split the touched blocks ------------------------------
+        const int32_t nsm = ld_vol(&ctl->n_small[cur]);
+        const unsigned long long bp = ld_vol(&ctl->big_pack[cur]);
+        const unsigned long long bp4 = ld_vol(&ctl->big_pack4[cur]);
+        const int32_t nbig = (int32_t)(bp >> 32), nch1 = (int32_t)(bp & 0xffffffffu);
+        const int32_t nch4 = (int32_t)(bp4 & 0xffffffffu);
+        if (ttid == 0) {
+            ctl->n_small[nxt] = 0;
+            ctl->big_pack[nxt] = 0ull;
+            ctl->big_pack4[nxt] = 0ull;
+            ctl->heavy[nxt] = 0;
+            ctl->items_last = nsm + nch1;
+        }
+        // chunk layout and pass count for this round (kernels_big.cuh)
+        const int mode_b = nsm + nch1 <= tnw ? 0 : (nsm + nch4 <= tnw ? 1 : 2);
+        const int32_t nch = mode_b == 0 ? nch1 : nch4;
+        for (int32_t it = tw; it < nsm + nch; it += tnw) {
+            int32_t cnt;
+            if (it < nsm) cnt = process_small<IDENT>(p, cur, round, C, p.small_list[it]);
+            else if (mode_b == 0) cnt = big_onepass<IDENT, 1>(p, cur, round, C, nbig, it - nsm);
+            else if (mode_b == 1) cnt = big_onepass<IDENT, kWide>(p, cur, round, C, nbig, it - nsm);
+            else cnt = big_tag<IDENT, kWide>(p, nbig, it - nsm);
+            if (lane == 0) my_members += (unsigned long long)cnt;
+        }
+        if (mode_b == 2) {
+            if (solo) __syncthreads();
+            else grid_barrier(p.bar, gen);
+            for (int32_t it = tw; it < nch; it += tnw) big_split<IDENT, kWide>(p, cur, round, C, nbig, it);
+        }
+        for (int k = threadIdx.x; k < kSeen; k += blockDim.x) s_seen[k] = -1;
+        if (solo) __syncthreads();
+        else grid_barrier(p.bar, gen);
+        if (tr) p.trace[round * 8 + 3] = globaltimer();
+        C = min(ld_vol(&ctl->next_min[cur]), ld_vol(&ctl->succ[cur]));
+        ++round;
+        if (cooldown > 0) --cooldown;
+        try_skip = p.allow_skip && cooldown == 0 && ld_vol(&ctl->heavy[cur]) == 0;
+
+
+        // ---- grid team: go solo for the next rounds? (uniform decision) ----
+        if (!solo && solo_ok && !try_skip && C != kBig && p.brange[C].y <= kSoloMaxC &&
+            ld_vol(&ctl->items_last) <= kSoloMaxItems) {
+            solo = true;  // CTA 0 continues alone, the others park at the loop head
+            fresh = true;
+            ++stretches;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        my_edges += __shfl_xor_sync(kFull, my_edges, o);
+        my_members += __shfl_xor_sync(kFull, my_members, o);
+    }
+    if (lane == 0) {
+        if (my_edges) atomicAdd(&ctl->work_edges, my_edges);
+        if (my_members) atomicAdd(&ctl->work_members, my_members);
+    }
+    if (gtid == 0) ctl->round = round;
+}

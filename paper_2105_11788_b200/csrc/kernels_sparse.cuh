@@ -78,6 +78,13 @@ struct SCtrl {
     int32_t skipcnt[2];                 // skip step: rounds retired
     int32_t skip_next[2];               // skip step: splitter after the window
     unsigned long long skipped_rounds;  // statistics
+    // solo stretches (kernels_loop.cuh)
+    unsigned wake;                      // hand-overs from CTA 0 back to the grid
+    unsigned parked;                    // park acknowledgements of the other CTAs
+    int32_t stop;                       // CTA 0 finished during a solo stretch
+    int32_t items_last;                 // phase-B work items of the last round
+    int32_t pub_try_skip, pub_cooldown, pub_backoff, pad2;
+    int64_t pub_skips;
 };
 
 // Window of unstable labels examined by one skip step (see k_refine_sparse).
@@ -125,7 +132,9 @@ struct SparseParams {
     unsigned long long* trace;  // optional: 4 globaltimer stamps per round (CTA 0)
     int64_t trace_rounds;
     int32_t allow_skip;         // retire runs of no-op rounds in one step
-    int32_t pad2;
+    int32_t cta_minor;          // spread consecutive work items over SMs
+    int32_t allow_solo;         // small rounds on CTA 0 alone (kernels_loop.cuh)
+    int32_t pad3;
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -404,238 +413,7 @@ __device__ __forceinline__ bool round_is_trivial(const SparseParams& p, int32_t 
 
 // ---- the persistent kernel ---------------------------------------------------
 
-template <bool IDENT>
-__global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParams p) {
-    SCtrl* ctl = p.ctrl;
-    const int lane = threadIdx.x & 31;
-    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    // logical warp id, CTA-minor: consecutive work items land on different
-    // SMs, so a small round's work is spread over the whole chip
-    const int32_t gwarp = (int32_t)((threadIdx.x >> 5) * gridDim.x + blockIdx.x);
-    const int32_t nwarps = (int32_t)(((int64_t)gridDim.x * blockDim.x) >> 5);
-    const int32_t aux_warp = nwarps - 1;  // keeps the unstable-set bookkeeping off phase A's work
-    unsigned gen = 0;
-    __shared__ int32_t s_seen[kSeen];
-    for (int k = threadIdx.x; k < kSeen; k += blockDim.x) s_seen[k] = -1;
-
-    if (gwarp == aux_warp) {
-        const int32_t c = u_next_warp(p, 0);
-        if (lane == 0) ctl->C0 = c;
-    }
-    if (gtid == 0) {
-        ctl->nontriv[0] = ctl->nontriv[1] = kBig;
-        ctl->skipcnt[0] = ctl->skipcnt[1] = 0;
-    }
-    grid_barrier(p.bar, gen);
-    int32_t C = ld_vol(&ctl->C0);
-    int64_t round = ld_vol(&ctl->round);
-    unsigned long long my_edges = 0, my_members = 0;
-    // no-op-round retirement (only in persistent mode: an observer must see
-    // every round): tried after a round that touched singleton blocks only,
-    // with exponential back-off when a try retires nothing
-    bool try_skip = false;
-    int32_t cooldown = 0, backoff = 16;
-    int64_t skips = 0;
-
-    for (int64_t done_here = 0;; ++done_here) {
-        if (done_here == p.round_limit) break;
-        const int64_t steps = (int64_t)p.A + round + 1;
-        if (p.has_guard && steps > p.max_supersteps) {
-            if (gtid == 0) {
-                ctl->error = 2;
-                ctl->guard_count = steps;
-            }
-            break;
-        }
-        if (C == kBig) {
-            if (gtid == 0) ctl->done = 1;
-            break;
-        }
-
-        // ---- skip step: retire the maximal run of no-op rounds -------------
-        // The next rounds' splitters are the unstable labels in increasing
-        // order; a no-op round only removes its splitter from the unstable
-        // set, so every unstable label below the first non-trivial one in
-        // the window [C, C + kSkipSpan) is retired at once (0 splits each).
-        if (try_skip && p.round_limit == INT64_MAX &&
-            (!p.has_guard || (int64_t)p.A + round + kSkipSpan + 1 <= p.max_supersteps)) {
-            const int sp = (int)(skips & 1);
-            const int32_t lim = (int64_t)C + kSkipSpan < (int64_t)p.n ? C + kSkipSpan : p.n;
-            for (int32_t w = (C >> 5) + gwarp; w <= ((lim - 1) >> 5); w += nwarps) {
-                const int32_t c = (w << 5) + lane;
-                const bool cand = c >= C && c < lim && ((ld_vol(&p.U0[w]) >> lane) & 1u);
-                if (cand && !round_is_trivial<IDENT>(p, c)) atomicMin(&ctl->nontriv[sp], c);
-            }
-            grid_barrier(p.bar, gen);
-            const int32_t nt = ld_vol(&ctl->nontriv[sp]);
-            const int32_t end = min(nt, lim);
-            int32_t cnt = 0;
-            if (end > C) {
-                const int32_t wlast = (end - 1) >> 5;
-                for (int64_t w = (C >> 5) + gtid; w <= wlast; w += (int64_t)gridDim.x * blockDim.x) {
-                    uint32_t v = ld_vol(&p.U0[w]);
-                    if (w == (C >> 5)) v &= ~0u << (C & 31);
-                    if (w == wlast && (end & 31)) v &= (1u << (end & 31)) - 1u;
-                    if (v) {
-                        atomicAnd(&p.U0[w], ~v);
-                        cnt += __popc(v);
-                    }
-                }
-            }
-            cnt = __reduce_add_sync(kFull, cnt);
-            if (lane == 0 && cnt) atomicAdd(&ctl->skipcnt[sp], cnt);
-            if (gwarp == aux_warp) {
-                const int32_t nx = nt < lim ? nt : u_next_warp(p, lim);
-                if (lane == 0) {
-                    ctl->skip_next[sp] = nx;
-                    ctl->nontriv[sp ^ 1] = kBig;
-                    ctl->skipcnt[sp ^ 1] = 0;
-                }
-            }
-            grid_barrier(p.bar, gen);
-            const int32_t retired = ld_vol(&ctl->skipcnt[sp]);
-            round += retired;
-            C = ld_vol(&ctl->skip_next[sp]);
-            ++skips;
-            if (gtid == 0) ctl->skipped_rounds += (unsigned long long)retired;
-            if (retired == 0) {
-                try_skip = false;
-                cooldown = backoff;
-                backoff = min(backoff * 2, 4096);
-            } else {
-                backoff = 16;
-            }
-            continue;
-        }
-
-        const int cur = (int)(round & 1), nxt = cur ^ 1;
-        const bool tr = p.trace != nullptr && gtid == 0 && round < p.trace_rounds;
-        if (tr) p.trace[round * 8 + 0] = globaltimer();
-
-        // ---- phase A --------------------------------------------------------
-        if (gwarp == aux_warp) {
-            u_clear_warp(p, C);
-            const int32_t sc = u_next_warp(p, C + 1);
-            if (lane == 0) {
-                ctl->succ[cur] = sc;
-                ctl->next_min[cur] = kBig;
-            }
-        }
-        {
-            const int2 cr = p.brange[C];
-            const int32_t cs = cr.x, cz = cr.y;
-            // members per warp: spread small splitters one member per warp so
-            // their in-edges are walked by as many warps as possible
-            const int32_t g = cz >= nwarps * 32 ? 32 : max(1, (cz + nwarps - 1) / nwarps);
-            for (int64_t i0 = (int64_t)gwarp * g; i0 < cz; i0 += (int64_t)nwarps * g) {
-                const int64_t i = i0 + lane;
-                int32_t e0 = 0, d = 0;
-                if (lane < g && i < cz) {
-                    const int32_t t = p.members[cs + i];
-                    e0 = p.rev_ptr[t];
-                    d = p.rev_ptr[t + 1] - e0;
-                }
-                int32_t incl = d;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int32_t y = __shfl_up_sync(kFull, incl, o);
-                    if (lane >= o) incl += y;
-                }
-                const int32_t total = __shfl_sync(kFull, incl, 31);
-                const int32_t excl = incl - d;
-                my_edges += (unsigned long long)d;
-                for (int32_t k0 = 0; k0 < total; k0 += 32) {
-                    const int32_t k = k0 + lane;
-                    // owner lane j: the last lane with excl_j <= k
-                    int32_t j = 0;
-#pragma unroll
-                    for (int step = 16; step; step >>= 1) {
-                        const int32_t ex = __shfl_sync(kFull, excl, j + step);
-                        if (ex <= k) j += step;
-                    }
-                    const int32_t ej = __shfl_sync(kFull, e0, j);
-                    const int32_t xj = __shfl_sync(kFull, excl, j);
-                    const bool act = k < total;
-                    int32_t s = 0;
-                    if (act) {
-                        const int32_t e = ej + (k - xj);
-                        if (IDENT) {
-                            s = p.rev_src[e];
-                            atomicOr(&p.mark[s >> 5], 1u << (s & 31));
-                        } else {
-                            const int2 r = p.rev[e];
-                            s = r.y;
-                            atomicOr(&p.mark[r.x >> 5], 1u << (r.x & 31));
-                            atomicOr(&p.touched[s >> 5], 1u << (s & 31));
-                        }
-                    }
-                    const int32_t b = act ? p.block[s] : 0;
-                    const unsigned same = __match_any_sync(kFull, act ? b : -1 - lane);
-                    const bool rep = act && lane == __ffs(same) - 1;
-                    if (rep && cta_first(s_seen, b)) {
-                        const uint32_t bit = 1u << (b & 31);
-                        if (!(ld_vol(&p.tblock[b >> 5]) & bit) && !(atomicOr(&p.tblock[b >> 5], bit) & bit))
-                            register_block(p, cur, b);
-                    }
-                }
-            }
-        }
-        if (tr) p.trace[round * 8 + 1] = globaltimer();
-        grid_barrier(p.bar, gen);
-        if (tr) {
-            p.trace[round * 8 + 2] = globaltimer();
-            p.trace[round * 8 + 4] = p.brange[C].y;
-            p.trace[round * 8 + 5] = my_edges;
-            p.trace[round * 8 + 6] = ld_vol(&ctl->n_small[cur]);
-            p.trace[round * 8 + 7] = ld_vol(&ctl->big_pack[cur]);
-        }
-
-        // ---- phase B --------------------------------------------------------
-        if (gtid == 0) {
-            ctl->n_small[nxt] = 0;
-            ctl->big_pack[nxt] = 0ull;
-            ctl->big_pack4[nxt] = 0ull;
-            ctl->heavy[nxt] = 0;
-        }
-        const int32_t nsm = ld_vol(&ctl->n_small[cur]);
-        const unsigned long long bp = ld_vol(&ctl->big_pack[cur]);
-        const unsigned long long bp4 = ld_vol(&ctl->big_pack4[cur]);
-        const int32_t nbig = (int32_t)(bp >> 32), nch1 = (int32_t)(bp & 0xffffffffu);
-        const int32_t nch4 = (int32_t)(bp4 & 0xffffffffu);
-        // chunk layout and pass count for this round (kernels_big.cuh)
-        const int mode_b = nsm + nch1 <= nwarps ? 0 : (nsm + nch4 <= nwarps ? 1 : 2);
-        const int32_t nch = mode_b == 0 ? nch1 : nch4;
-        for (int32_t it = gwarp; it < nsm + nch; it += nwarps) {
-            int32_t cnt;
-            if (it < nsm) cnt = process_small<IDENT>(p, cur, round, C, p.small_list[it]);
-            else if (mode_b == 0) cnt = big_onepass<IDENT, 1>(p, cur, round, C, nbig, it - nsm);
-            else if (mode_b == 1) cnt = big_onepass<IDENT, kWide>(p, cur, round, C, nbig, it - nsm);
-            else cnt = big_tag<IDENT, kWide>(p, nbig, it - nsm);
-            if (lane == 0) my_members += (unsigned long long)cnt;
-        }
-        if (mode_b == 2) {
-            grid_barrier(p.bar, gen);
-            for (int32_t it = gwarp; it < nch; it += nwarps) big_split<IDENT, kWide>(p, cur, round, C, nbig, it);
-        }
-        for (int k = threadIdx.x; k < kSeen; k += blockDim.x) s_seen[k] = -1;
-        grid_barrier(p.bar, gen);
-        if (tr) p.trace[round * 8 + 3] = globaltimer();
-        C = min(ld_vol(&ctl->next_min[cur]), ld_vol(&ctl->succ[cur]));
-        ++round;
-        if (cooldown > 0) --cooldown;
-        try_skip = p.allow_skip && cooldown == 0 && ld_vol(&ctl->heavy[cur]) == 0;
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        my_edges += __shfl_xor_sync(kFull, my_edges, o);
-        my_members += __shfl_xor_sync(kFull, my_members, o);
-    }
-    if (lane == 0) {
-        if (my_edges) atomicAdd(&ctl->work_edges, my_edges);
-        if (my_members) atomicAdd(&ctl->work_members, my_members);
-    }
-    if (gtid == 0) ctl->round = round;
-}
+#include "kernels_loop.cuh"
 
 // ---- setup kernels -----------------------------------------------------------
 

@@ -324,3 +324,28 @@ def test_noop_round_retirement_is_exact(monkeypatch):
         monkeypatch.delenv("BISIM_NO_SKIP")
         assert np.array_equal(b1, b2), inst.name
         assert s1 == s2, inst.name
+
+
+@pytest.mark.parametrize("env", ["BISIM_NO_SOLO", "BISIM_NO_SKIP", "BISIM_CTA_MAJOR"])
+def test_loop_variants_identical(env, monkeypatch):
+    """Solo stretches, no-op retirement and work placement never change a
+    result: every variant reproduces the oracle on mixed workloads."""
+    insts = [W.c2_kripke(n=30000, out_degree=4, seed=8), W.fanout(2000),
+             W.lifted_quotient(60000, 600, 12, 4, 3, 2, seed=9)]
+    g = np.random.default_rng(31)
+    n, m, A = 20000, 80000, 3
+    insts.append(W.Instance("rand", "bcrp", n, g.integers(0, n, m, dtype=np.int32),
+                            g.integers(0, n, m, dtype=np.int32), g.integers(0, A, m, dtype=np.int32), A))
+    for inst in insts:
+        if inst.kind == "bcrp":
+            res = oracle.bcrp(inst.n, inst.src, inst.act, inst.dst, inst.num_actions, threads=8)
+            run = lambda: bcrp_arrays(inst.n, inst.src, inst.act, inst.dst, inst.num_actions)
+        else:
+            res = oracle.rcpp(inst.n, inst.src, inst.dst, inst.pi0, threads=8)
+            run = lambda: rcpp_arrays(inst.n, inst.src, inst.dst, inst.pi0)
+        b1, s1, _ = run()
+        _same_oracle(b1, s1, res, inst.name)
+        monkeypatch.setenv(env, "1")
+        b2, s2, _ = run()
+        monkeypatch.delenv(env)
+        _same_oracle(b2, s2, res, inst.name + " " + env)
