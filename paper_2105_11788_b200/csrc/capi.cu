@@ -396,7 +396,7 @@ int run(Job& j) {
         lp.ctrl = ctrl;
     } else {
         // members grouped by block: counting sort of states by label
-        int32_t* members = (int32_t*)c.members.ensure((int64_t)n * 4);
+        MemberRec* members = (MemberRec*)c.members.ensure((int64_t)n * sizeof(MemberRec));
         int32_t* bstart = (int32_t*)c.bstart.ensure(((int64_t)n + 1) * 4);
         int32_t* bsize = (int32_t*)c.bsize.ensure((int64_t)n * 4);
         CK(cudaMemsetAsync(bstart, 0, ((int64_t)n + 1) * 4, st));
@@ -408,7 +408,8 @@ int run(Job& j) {
         int2* brange = (int2*)c.brange.ensure((int64_t)n * 8);
         k_pack_ranges<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, bstart, bsize, brange);
         ++c.launches;
-        k_fill_members<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, block, cursor, members);
+        k_fill_members<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, block, cursor, j.bcrp ? off : nullptr, rev_ptr,
+                                                              members);
         ++c.launches;
         uint32_t* U1 = U + nw0;
         uint32_t* U2 = U1 + nw1 + 1;
@@ -447,7 +448,7 @@ int run(Job& j) {
         sp.big_base = (int32_t*)c.big_base.ensure(((int64_t)n / 32 + 2) * 4);
         sp.big_list4 = (int4*)c.big_list4.ensure(((int64_t)n / 32 + 2) * 16);
         sp.big_base4 = (int32_t*)c.big_base4.ensure(((int64_t)n / 32 + 2) * 4);
-        sp.tmp = (int32_t*)c.tmp.ensure((int64_t)n * 4);
+        sp.tmp = (MemberRec*)c.tmp.ensure((int64_t)n * sizeof(MemberRec));
         sp.scnt = (int32_t*)c.scnt.ensure((int64_t)n * 4);
         sp.smin = (int32_t*)c.smin.ensure((int64_t)n * 4);
         sp.kcur = (int32_t*)c.kcur.ensure((int64_t)n * 4);

@@ -49,76 +49,74 @@ __device__ __forceinline__ int32_t find_owner(const SparseParams& p, int32_t nbi
     return lo + 31 - __clz(b);
 }
 
+// A lane's members of a chunk.  Slot base comes with the record; the slot
+// count is the leader's (members share the leader's label set, bcrp.py:16-19).
 template <int K>
 struct ChunkLane {
-    int32_t u[K];
-    int32_t ou[K];
-    int32_t nr[K];
+    MemberRec r[K];
     bool valid[K];
     bool sp[K];
     bool tu[K];
 };
 
+// slot base / slot count of member record r (RCPP: one slot per state)
+template <bool IDENT>
+__device__ __forceinline__ int32_t slot_base(const MemberRec& r) {
+    return IDENT ? r.x : r.y;
+}
+
 // Tag a chunk's members.  Loads are staged across the lane's members
-// (member ids, then touched bits and slot offsets, then mark words) so the
-// K dependency chains overlap instead of running back to back.
+// (records, then touched bits, then mark words) so the K dependency chains
+// overlap instead of running back to back.
 template <bool IDENT, int K>
 __device__ __forceinline__ void chunk_tag(const SparseParams& p, int32_t l, int32_t bs, int32_t bz,
-                                          int32_t ci0, ChunkLane<K>& c) {
+                                          int32_t ci0, int32_t ol, int32_t nrl, ChunkLane<K>& c) {
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         const int32_t i = ci0 + 32 * j + lane;
         c.valid[j] = i < bz;
-        c.u[j] = c.valid[j] ? p.members[bs + i] : 0;
+        c.r[j] = c.valid[j] ? p.members[bs + i] : make_int4(0, 0, 0, 0);
     }
     if (IDENT) {
         const bool tl = get_bit(p.mark, l);
         uint32_t mw[K];
 #pragma unroll
-        for (int j = 0; j < K; ++j) mw[j] = c.valid[j] ? p.mark[c.u[j] >> 5] : 0u;
+        for (int j = 0; j < K; ++j) mw[j] = c.valid[j] ? p.mark[c.r[j].x >> 5] : 0u;
 #pragma unroll
         for (int j = 0; j < K; ++j) {
-            c.tu[j] = (mw[j] >> (c.u[j] & 31)) & 1u;
-            c.ou[j] = c.u[j];
-            c.nr[j] = 1;
-            c.sp[j] = c.valid[j] && c.u[j] != l && c.tu[j] != tl;
+            c.tu[j] = (mw[j] >> (c.r[j].x & 31)) & 1u;
+            c.sp[j] = c.valid[j] && c.r[j].x != l && c.tu[j] != tl;
         }
         return;
     }
-    const int32_t ol = p.off[l], nrl = p.off[l + 1] - ol;
     const bool tl = get_bit(p.touched, l);
-    uint32_t tw[K];
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-        tw[j] = c.valid[j] ? p.touched[c.u[j] >> 5] : 0u;
-        c.ou[j] = c.valid[j] ? p.off[c.u[j]] : 0;
-        c.nr[j] = c.valid[j] ? p.off[c.u[j] + 1] - c.ou[j] : 0;
-    }
-    // members share the leader's label set, hence its slot count (bcrp.py:16-19)
     const uint32_t lb = (nrl > 0 && nrl <= 32) ? get_bits(p.mark, ol, nrl) : 0u;
-    uint32_t wa[K], wb[K];
-    bool need[K];
+    uint32_t tw[K], wa[K], wb[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-        c.tu[j] = (tw[j] >> (c.u[j] & 31)) & 1u;
-        need[j] = c.valid[j] && c.u[j] != l && (c.tu[j] || tl) && c.nr[j] > 0;
-        const int32_t w0 = c.ou[j] >> 5, sh = c.ou[j] & 31;
-        wa[j] = need[j] ? p.mark[w0] : 0u;
-        wb[j] = (need[j] && sh + c.nr[j] > 32) ? p.mark[w0 + 1] : 0u;
+        // touched word and the member's mark words in one wave of loads;
+        // the mark words are only needed when a mark can differ
+        tw[j] = c.valid[j] ? p.touched[c.r[j].x >> 5] : 0u;
+        const int32_t ou = c.r[j].y, w0 = ou >> 5, sh = ou & 31;
+        const bool maybe = c.valid[j] && c.r[j].x != l && nrl > 0 && nrl <= 32;
+        wa[j] = maybe ? p.mark[w0] : 0u;
+        wb[j] = (maybe && sh + nrl > 32) ? p.mark[w0 + 1] : 0u;
     }
 #pragma unroll
     for (int j = 0; j < K; ++j) {
+        c.tu[j] = (tw[j] >> (c.r[j].x & 31)) & 1u;
+        const bool need = c.valid[j] && c.r[j].x != l && (c.tu[j] || tl) && nrl > 0;
         bool sp = false;
-        if (need[j]) {
-            const int32_t nr = c.nr[j], sh = c.ou[j] & 31;
-            if (nr <= 32) {
+        if (need) {
+            const int32_t ou = c.r[j].y, sh = ou & 31;
+            if (nrl <= 32) {
                 uint32_t v = wa[j] >> sh;
-                if (sh + nr > 32) v |= wb[j] << (32 - sh);
-                if (nr < 32) v &= (1u << nr) - 1u;
+                if (sh + nrl > 32) v |= wb[j] << (32 - sh);
+                if (nrl < 32) v &= (1u << nrl) - 1u;
                 sp = v != lb;
             } else {
-                sp = slots_differ(p.mark, c.ou[j], ol, nr);
+                sp = slots_differ(p.mark, ou, ol, nrl);
             }
         }
         c.sp[j] = sp;
@@ -136,13 +134,13 @@ __device__ __forceinline__ void chunk_counts(const ChunkLane<K>& c, unsigned* ba
         kb[j] = __ballot_sync(kFull, c.valid[j] && !c.sp[j]);
         nsplit += __popc(bal[j]);
         nkeep += __popc(kb[j]);
-        if (c.sp[j]) m = min(m, c.u[j]);
+        if (c.sp[j]) m = min(m, c.r[j].x);
     }
     wmin = __reduce_min_sync(kFull, m);
 }
 
-// Move the chunk's members to their compacted positions (keep part first,
-// split part at the tail of the block range) and relabel split members.
+// Move the chunk's member records to their compacted positions (keep part
+// first, split part at the tail of the block range); relabel split members.
 template <int K>
 __device__ __forceinline__ void chunk_compact(const SparseParams& p, int32_t l, int32_t bs, int32_t bz,
                                               int32_t ns, int32_t w, const ChunkLane<K>& c,
@@ -162,8 +160,8 @@ __device__ __forceinline__ void chunk_compact(const SparseParams& p, int32_t l, 
     for (int j = 0; j < K; ++j) {
         if (c.valid[j]) {
             const int32_t np = c.sp[j] ? bs + keep + sbase + __popc(bal[j] & lt) : bs + kbase + __popc(kb[j] & lt);
-            p.members[np] = c.u[j];
-            if (c.sp[j]) p.block[c.u[j]] = w;
+            p.members[np] = c.r[j];
+            if (c.sp[j]) p.block[c.r[j].x] = w;
         }
         sbase += __popc(bal[j]);
         kbase += __popc(kb[j]);
@@ -177,17 +175,34 @@ __device__ __forceinline__ void finish_block(const SparseParams& p, int cur, int
     raise_split(p, cur, round, l, w, C);
 }
 
+template <bool IDENT>
+__device__ __forceinline__ void leader_slots(const SparseParams& p, int32_t l, int32_t& ol, int32_t& nrl) {
+    if (IDENT) {
+        ol = l;
+        nrl = 1;
+    } else {
+        ol = p.off[l];
+        nrl = p.off[l + 1] - ol;
+    }
+}
+
 // two-pass, sub-phase 1: tag split members, accumulate count and minimum
 template <bool IDENT, int K>
 __device__ int32_t big_tag(const SparseParams& p, int32_t nbig, int32_t ci) {
     const int lane = threadIdx.x & 31;
     const int4 e = big_list_of<K>(p)[find_owner<K>(p, nbig, ci)];
     const int32_t l = e.x, bs = e.y, bz = e.z, ci0 = (ci - e.w) * (32 * K);
+    int32_t ol, nrl;
+    leader_slots<IDENT>(p, l, ol, nrl);
     ChunkLane<K> c;
-    chunk_tag<IDENT, K>(p, l, bs, bz, ci0, c);
+    chunk_tag<IDENT, K>(p, l, bs, bz, ci0, ol, nrl, c);
 #pragma unroll
-    for (int j = 0; j < K; ++j)
-        if (c.valid[j]) p.tmp[bs + ci0 + 32 * j + lane] = c.sp[j] ? -1 - c.u[j] : c.u[j];
+    for (int j = 0; j < K; ++j) {
+        if (!c.valid[j]) continue;
+        MemberRec t = c.r[j];
+        if (c.sp[j]) t.x = -1 - t.x;
+        p.tmp[bs + ci0 + 32 * j + lane] = t;
+    }
     unsigned bal[K], kb[K];
     int32_t nsplit, nkeep, wmin;
     chunk_counts<K>(c, bal, kb, nsplit, nkeep, wmin);
@@ -205,15 +220,22 @@ __device__ void big_split(const SparseParams& p, int cur, int64_t round, int32_t
     const int lane = threadIdx.x & 31;
     const int4 e = big_list_of<K>(p)[find_owner<K>(p, nbig, ci)];
     const int32_t l = e.x, bs = e.y, bz = e.z, ci0 = (ci - e.w) * (32 * K);
+    int32_t ol, nrl;
+    leader_slots<IDENT>(p, l, ol, nrl);
     ChunkLane<K> c;
+    uint32_t tw[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         const int32_t i = ci0 + 32 * j + lane;
         c.valid[j] = i < bz;
-        const int32_t code = c.valid[j] ? p.tmp[bs + i] : 0;
-        c.sp[j] = c.valid[j] && code < 0;
-        c.u[j] = c.sp[j] ? -1 - code : code;
+        MemberRec t = c.valid[j] ? p.tmp[bs + i] : make_int4(0, 0, 0, 0);
+        c.sp[j] = c.valid[j] && t.x < 0;
+        if (c.sp[j]) t.x = -1 - t.x;
+        c.r[j] = t;
     }
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+        tw[j] = c.valid[j] ? (IDENT ? p.mark[c.r[j].x >> 5] : p.touched[c.r[j].x >> 5]) : 0u;
     const int32_t ns = p.scnt[l];
     if (ns) {
         unsigned bal[K], kb[K];
@@ -226,21 +248,8 @@ __device__ void big_split(const SparseParams& p, int cur, int64_t round, int32_t
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         if (!c.valid[j]) continue;
-        const int32_t u = c.u[j];
-        bool tu;
-        int32_t ou = 0, nr = 0;
-        if (IDENT) {
-            tu = get_bit(p.mark, u);
-            ou = u;
-            nr = 1;
-        } else {
-            tu = get_bit(p.touched, u);
-            if (tu) {
-                ou = p.off[u];
-                nr = p.off[u + 1] - ou;
-            }
-        }
-        clear_member<IDENT>(p, u, tu, ou, nr);
+        const bool tu = (tw[j] >> (c.r[j].x & 31)) & 1u;
+        clear_member<IDENT>(p, c.r[j].x, tu, slot_base<IDENT>(c.r[j]), nrl);
     }
     if (ci0 == 0 && lane == 0) atomicAnd(&p.tblock[l >> 5], ~(1u << (l & 31)));
 }
@@ -252,8 +261,10 @@ __device__ int32_t big_onepass(const SparseParams& p, int cur, int64_t round, in
     const int lane = threadIdx.x & 31;
     const int4 e = big_list_of<K>(p)[find_owner<K>(p, nbig, ci)];
     const int32_t l = e.x, bs = e.y, bz = e.z, ci0 = (ci - e.w) * (32 * K);
+    int32_t ol, nrl;
+    leader_slots<IDENT>(p, l, ol, nrl);
     ChunkLane<K> c;
-    chunk_tag<IDENT, K>(p, l, bs, bz, ci0, c);
+    chunk_tag<IDENT, K>(p, l, bs, bz, ci0, ol, nrl, c);
     unsigned bal[K], kb[K];
     int32_t nsplit, nkeep, wmin;
     chunk_counts<K>(c, bal, kb, nsplit, nkeep, wmin);
@@ -265,8 +276,8 @@ __device__ int32_t big_onepass(const SparseParams& p, int cur, int64_t round, in
                 atomicAdd(&p.scnt[l], nsplit);
                 atomicMin(&p.smin[l], wmin);
             }
-            __threadfence();
-            atomicAdd(&p.sarr[l], 1);
+            // release: the count/minimum above are visible before the arrival
+            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(&p.sarr[l]) : "memory");
             while (ld_acquire_u32((const unsigned*)&p.sarr[l]) < (unsigned)nch_b) {
             }
             ns = ld_vol(&p.scnt[l]);
@@ -283,8 +294,7 @@ __device__ int32_t big_onepass(const SparseParams& p, int cur, int64_t round, in
     // arrival count above is complete (or the block is a single chunk)
 #pragma unroll
     for (int j = 0; j < K; ++j)
-        if (c.valid[j]) clear_member<IDENT>(p, c.u[j], c.tu[j], c.ou[j], c.nr[j]);
+        if (c.valid[j]) clear_member<IDENT>(p, c.r[j].x, c.tu[j], slot_base<IDENT>(c.r[j]), nrl);
     if (ci0 == 0 && lane == 0) atomicAnd(&p.tblock[l >> 5], ~(1u << (l & 31)));
     return min(32 * K, bz - ci0);
 }
-

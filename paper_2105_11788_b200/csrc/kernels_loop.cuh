@@ -219,9 +219,9 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
                 const int64_t i = i0 + lane;
                 int32_t e0 = 0, d = 0;
                 if (lane < g && i < cz) {
-                    const int32_t t = p.members[cs + i];
-                    e0 = p.rev_ptr[t];
-                    d = p.rev_ptr[t + 1] - e0;
+                    const MemberRec r = p.members[cs + i];
+                    e0 = r.z;
+                    d = r.w - r.z;
                 }
                 int32_t incl = d;
 #pragma unroll

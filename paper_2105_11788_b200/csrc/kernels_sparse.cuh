@@ -92,6 +92,12 @@ constexpr int32_t kSkipSpan = 32768;
 constexpr int32_t kSkipMaxEdges = 256;
 constexpr int kWide = 4;  // members per lane in the wide big-block chunk layout (kernels_big.cuh)
 
+// A member record carries what the phases read right after the member id,
+// so one 16-byte load replaces two dependent ones: (state u, slot base
+// off[u] (BCRP; unused for RCPP), in-edge range [e0, e1) of u in the
+// reverse CSR).  Records move with their state when a block is compacted.
+using MemberRec = int4;
+
 struct SparseParams {
     int32_t n;
     int32_t A;
@@ -105,7 +111,7 @@ struct SparseParams {
     const int2* __restrict__ rev;          // BCRP in-edges: (slot, source)
     const int32_t* __restrict__ rev_src;   // RCPP in-edges: source (= slot)
     int32_t* block;
-    int32_t* members;   // states grouped by block
+    int4* members;      // member records grouped by block (see MemberRec)
     int2* brange;       // (start, size) of block `label` in members (valid for leaders)
     uint32_t* mark;     // L-bit mark bitmap
     uint32_t* touched;  // n-bit: state has a marked slot this round (BCRP)
@@ -120,7 +126,7 @@ struct SparseParams {
     int32_t* big_base;    // first chunk of each big touched block (ascending)
     int4* big_list4;      // the same blocks in the kWide chunk layout
     int32_t* big_base4;
-    int32_t* tmp;         // per member position: member, or -1-member if split
+    int4* tmp;            // per member position: the record, x = -1-state if split
     int32_t* scnt;        // per label: split count / min split / compaction cursors
     int32_t* smin;
     int32_t* kcur;
@@ -293,9 +299,13 @@ __device__ __forceinline__ bool cta_first(int32_t* seen, int32_t b) {
 
 // ---- phase B helpers --------------------------------------------------------
 
+// Split test of member record r against its leader l (slot base ol, nrl
+// slots: members share the leader's label set, hence its slot count,
+// bcrp.py:16-19).
 template <bool IDENT>
-__device__ __forceinline__ bool member_splits(const SparseParams& p, int32_t u, int32_t l,
-                                              bool tl, bool& tu, int32_t& ou, int32_t& nr) {
+__device__ __forceinline__ bool member_splits(const SparseParams& p, MemberRec r, int32_t l, bool tl,
+                                              int32_t ol, int32_t nrl, bool& tu, int32_t& ou, int32_t& nr) {
+    const int32_t u = r.x;
     if (IDENT) {
         tu = get_bit(p.mark, u);
         ou = u;
@@ -303,10 +313,10 @@ __device__ __forceinline__ bool member_splits(const SparseParams& p, int32_t u, 
         return u != l && (tu != tl);
     }
     tu = get_bit(p.touched, u);
-    ou = p.off[u];
-    nr = p.off[u + 1] - ou;
+    ou = r.y;
+    nr = nrl;
     if (u == l || !(tu || tl) || nr == 0) return false;
-    return slots_differ(p.mark, ou, p.off[l], nr);
+    return slots_differ(p.mark, ou, ol, nr);
 }
 
 template <bool IDENT>
@@ -347,11 +357,13 @@ __device__ int32_t process_small(const SparseParams& p, int cur, int64_t round, 
     const int lane = threadIdx.x & 31;
     const int32_t l = e.x, bs = e.y, bz = e.z;
     const bool valid = lane < bz;
-    const int32_t u = valid ? p.members[bs + lane] : -1;
+    const MemberRec rec = valid ? p.members[bs + lane] : make_int4(-1, 0, 0, 0);
+    const int32_t u = rec.x;
     const bool tl = IDENT ? get_bit(p.mark, l) : get_bit(p.touched, l);
+    const int32_t ol = IDENT ? l : p.off[l], nrl = IDENT ? 1 : p.off[l + 1] - ol;
     bool tu = false;
     int32_t ou = 0, nr = 0;
-    const bool sp = valid && member_splits<IDENT>(p, u, l, tl, tu, ou, nr);
+    const bool sp = valid && member_splits<IDENT>(p, rec, l, tl, ol, nrl, tu, ou, nr);
     const unsigned bal = __ballot_sync(kFull, sp);
     if (bal) {
         const int32_t ns = __popc(bal);
@@ -361,7 +373,7 @@ __device__ int32_t process_small(const SparseParams& p, int cur, int64_t round, 
         const unsigned vmask = bz >= 32 ? kFull : ((1u << bz) - 1u);
         if (valid) {
             const int32_t np = sp ? bs + keep + __popc(bal & lt) : bs + __popc(~bal & vmask & lt);
-            p.members[np] = u;
+            p.members[np] = rec;
             if (sp) p.block[u] = w;
         }
         if (lane == 0) {
@@ -392,8 +404,8 @@ __device__ __forceinline__ bool round_is_trivial(const SparseParams& p, int32_t 
     if (r.y > 32) return false;
     int32_t budget = kSkipMaxEdges;
     for (int32_t i = 0; i < r.y; ++i) {
-        const int32_t t = p.members[r.x + i];
-        const int32_t e0 = p.rev_ptr[t], e1 = p.rev_ptr[t + 1];
+        const MemberRec mr = p.members[r.x + i];
+        const int32_t e0 = mr.z, e1 = mr.w;
         if (e1 - e0 > budget) return false;
         budget -= e1 - e0;
         for (int32_t e = e0; e < e1; e += 4) {
@@ -429,7 +441,8 @@ __global__ void k_block_sizes(int32_t n, const int32_t* __restrict__ block, int3
 }
 
 __global__ void k_fill_members(int32_t n, const int32_t* __restrict__ block, int32_t* cursor,
-                               int32_t* members) {
+                               const int32_t* __restrict__ off, const int32_t* __restrict__ rev_ptr,
+                               MemberRec* members) {
     const int lane = threadIdx.x & 31;
     for (int64_t s0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); s0 < n;
          s0 += (int64_t)gridDim.x * blockDim.x) {
@@ -440,7 +453,9 @@ __global__ void k_fill_members(int32_t n, const int32_t* __restrict__ block, int
         int32_t base = 0;
         if (s < n && lane == leader) base = atomicAdd(&cursor[b], __popc(g));
         base = __shfl_sync(kFull, base, leader);
-        if (s < n) members[base + __popc(g & lanemask_lt())] = (int32_t)s;
+        if (s < n)
+            members[base + __popc(g & lanemask_lt())] =
+                make_int4((int32_t)s, off ? off[s] : 0, rev_ptr[s], rev_ptr[s + 1]);
     }
 }
 
