@@ -111,6 +111,42 @@ __device__ __forceinline__ bool slots_differ(const uint32_t* mark, int32_t os, i
 // transition labelled 64 w + b.  Word-major so each label round reads one
 // coalesced plane.  Validates transitions (lts.py:47-52).  Warp-aggregated:
 // lanes hitting the same mask word OR their bits together first.
+// Runs of equal keys on consecutive lanes.  Transition files are usually
+// grouped by source, so such runs collapse to one atomic each; on random
+// input this costs a shuffle and a ballot (cheaper than __match_any_sync).
+struct LaneRun {
+    int leader;  // first lane of my run
+    int rank;    // my position in the run
+    int len;     // run length
+    int next;    // first lane after my run
+};
+
+template <typename T>
+__device__ __forceinline__ LaneRun lane_run(T key) {
+    const int lane = threadIdx.x & 31;
+    const T prev = __shfl_up_sync(kFull, key, 1);
+    const unsigned starts = __ballot_sync(kFull, lane == 0 || prev != key);
+    const unsigned le = (2u << lane) - 1u;  // lanes <= me (wraps to all lanes for lane 31)
+    LaneRun r;
+    r.leader = 31 - __clz(starts & le);
+    r.rank = lane - r.leader;
+    const unsigned after = starts & ~le;
+    r.next = after ? __ffs(after) - 1 : 32;
+    r.len = r.next - r.leader;
+    return r;
+}
+
+// OR of v over my run, valid in the run's leader lane
+__device__ __forceinline__ unsigned long long run_or(unsigned long long v, const LaneRun& r) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned long long o = __shfl_down_sync(kFull, v, d);
+        if (lane + d < r.next) v |= o;
+    }
+    return v;
+}
+
 __global__ void k_label_mask(int32_t n, int64_t m, int32_t A, const int32_t* __restrict__ src,
                              const int32_t* __restrict__ act, const int32_t* __restrict__ dst,
                              unsigned long long* lmask, Ctrl* ctrl) {
@@ -130,11 +166,9 @@ __global__ void k_label_mask(int32_t n, int64_t m, int32_t A, const int32_t* __r
                 ctrl->bad = 1;
             }
         }
-        const unsigned grp = __match_any_sync(kFull, addr);
-        const unsigned lo = __reduce_or_sync(grp, (unsigned)bits);
-        const unsigned hi = __reduce_or_sync(grp, (unsigned)(bits >> 32));
-        if (ok && lane == __ffs(grp) - 1)
-            atomicOr(&lmask[addr], ((unsigned long long)hi << 32) | lo);
+        const LaneRun r = lane_run(addr);
+        bits = run_or(bits, r);
+        if (ok && r.rank == 0) atomicOr(&lmask[addr], bits);
     }
 }
 
@@ -190,8 +224,8 @@ __global__ void k_indeg(int64_t m, const int32_t* __restrict__ dst, int32_t* cnt
     for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < m; i0 += stride) {
         const int64_t i = i0 + lane;
         const int32_t t = i < m ? dst[i] : -1 - lane;
-        const unsigned grp = __match_any_sync(kFull, t);
-        if (i < m && lane == __ffs(grp) - 1) atomicAdd(&cnt[t], __popc(grp));
+        const LaneRun r = lane_run(t);
+        if (i < m && r.rank == 0) atomicAdd(&cnt[t], r.len);
     }
 }
 

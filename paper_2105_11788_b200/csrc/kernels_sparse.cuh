@@ -499,13 +499,12 @@ __global__ void k_rev_fill2(int32_t n, int64_t m, const int32_t* __restrict__ sr
             s = src[i];
             slot = BCRP ? off[s] + label_rank(lmask, n, s, act[i]) : s;
         }
-        const unsigned grp = __match_any_sync(kFull, t);
-        const int leader = __ffs(grp) - 1;
+        const LaneRun run = lane_run(t);
         int32_t base = 0;
-        if (i < m && lane == leader) base = atomicAdd(&cursor[t], __popc(grp));
-        base = __shfl_sync(kFull, base, leader);
+        if (i < m && run.rank == 0) base = atomicAdd(&cursor[t], run.len);
+        base = __shfl_sync(kFull, base, run.leader);
         if (i < m) {
-            const int32_t at = base + __popc(grp & lanemask_lt());
+            const int32_t at = base + run.rank;
             if (BCRP) rev[at] = make_int2(slot, s);
             else rev_src[at] = s;
         }
