@@ -135,6 +135,54 @@ int bisim_preprocess(int32_t n, int64_t m, int32_t num_actions, const int32_t *s
 int bisim_label_partition(int32_t n, int64_t m, int32_t num_actions, const int32_t *src,
                           const int32_t *act, int32_t *block_out, int device);
 
+/* ---- the steps either side of the path ------------------ */
+/* quotient(lts, partition) (aut.py:132-152): one state per block, blocks
+ * numbered densely in increasing leader order, duplicate (block, action,
+ * block) transitions merged keeping first occurrences in transition order.
+ * block is a leader-form partition (lts.py:88-94, else BISIM_BAD_INPUT).
+ * q_src/q_act/q_dst hold at least m entries; *q_m <= m transitions are
+ * written.  Host pointers. */
+int bisim_quotient(int32_t n, int64_t m, int32_t num_actions, const int32_t *src,
+                   const int32_t *act, const int32_t *dst, const int32_t *block,
+                   int32_t initial_state, int32_t *q_n, int64_t *q_m, int32_t *q_src,
+                   int32_t *q_act, int32_t *q_dst, int32_t *q_initial, int device);
+
+/* is_stable(lts, partition) (oracle.py:128-141): *stable_out = 1 iff every
+ * state sees the same set of (action, target block) pairs as its leader. */
+int bisim_is_stable(int32_t n, int64_t m, int32_t num_actions, const int32_t *src,
+                    const int32_t *act, const int32_t *dst, const int32_t *block,
+                    int32_t *stable_out, int device);
+
+/* partition_from_assignment(assignment) (lts.py:117-128): states sharing an
+ * id share a block, whose leader is its smallest state. */
+int bisim_canonical(int32_t n, const int64_t *assignment, int32_t *block_out, int device);
+
+/* ---- .aut ingestion (aut.py:79-92) ---------------- */
+/* parse_aut(text): header "des (<initial>, <m>, <n>)" then m lines
+ * "(<source>, <label>, <target>)"; action ids follow the sorted label
+ * strings (lts.py:69-70).  Multi-threaded host C++ (threads <= 0: all
+ * cores).  On a malformed input returns BISIM_BAD_INPUT, bisim_last_error()
+ * holds the reference's ParseError message without its "line N: " prefix
+ * and info->error_line holds N (0 when the error has no line). */
+typedef struct bisim_aut bisim_aut;
+typedef struct bisim_aut_info {
+    int32_t n;
+    int32_t initial_state;
+    int64_t m;
+    int32_t num_actions;
+    int32_t pad;
+    int64_t error_line;
+} bisim_aut_info;
+int bisim_aut_parse(const char *text, int64_t len, int32_t threads, bisim_aut **out,
+                    bisim_aut_info *info);
+/* Same, reading (mmap) a file. */
+int bisim_aut_read_file(const char *path, int32_t threads, bisim_aut **out, bisim_aut_info *info);
+/* Copies the m transitions into caller arrays of info->m entries. */
+int bisim_aut_columns(const bisim_aut *aut, int32_t *src, int32_t *act, int32_t *dst);
+/* Label of action id `action` (UTF-8, *len bytes, not NUL-terminated). */
+const char *bisim_aut_label(const bisim_aut *aut, int32_t action, int64_t *len);
+void bisim_aut_free(bisim_aut *aut);
+
 /* ---- misc ---------------------------------------------------------------- */
 const char *bisim_last_error(void);
 int bisim_device_count(void);

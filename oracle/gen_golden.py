@@ -8,6 +8,8 @@ can check against them.
     python oracle/gen_golden.py cases      # small known-answer instances
     python oracle/gen_golden.py sweep      # acceptance-sweep instances
     python oracle/gen_golden.py c1         # config c1 full run (~35 min, 1 core)
+    python oracle/gen_golden.py post       # quotient / is_stable / canonical fixtures
+    python oracle/gen_golden.py aut        # parse_aut outcomes (texts + results / errors)
 
 Every fixture records the instance (src/act/dst arrays or the generator
 recipe), the reference's Priority-policy outputs (block array in leader form,
@@ -251,7 +253,135 @@ def c1():
     print("c1:", meta)
 
 
+def post(count=400):
+    """quotient (aut.py:132-152), is_stable (oracle.py:128-141) and
+    partition_from_assignment (lts.py:117-128) of the reference, on the first
+    `count` sweep instances and the medium instances, each under several
+    partitions (the coarsest one, the label partition, trivial, discrete and
+    a random one), plus random id assignments."""
+    pb = _ref()
+    from parbisim.oracle import is_stable as ref_is_stable
+    with gzip.open(os.path.join(OUT, "sweep.json.gz"), "rt") as fh:
+        sweep_recs = json.load(fh)[:count]
+    with gzip.open(os.path.join(OUT, "cases.json.gz"), "rt") as fh:
+        case_recs = json.load(fh)["medium_random"]
+    rng = random.Random(31337)
+    out = []
+    for idx, rec in enumerate(sweep_recs + case_recs):
+        n, A = rec["n"], rec["num_actions"]
+        init = rng.randrange(n)
+        lts = pb.Lts(n=n, action_labels=tuple(f"a{k}" for k in range(A)),
+                     transitions=tuple(pb.Transition(s, a, t) for s, a, t in
+                                       zip(rec["src"], rec["act"], rec["dst"])),
+                     initial_state=init)
+        k = rng.randint(1, max(1, n // 2))
+        assignment = [rng.randrange(k) * 7 - 3 for _ in range(n)]
+        parts = {"coarsest": rec["bcrp"]["block"],
+                 "labels": list(pb.partition_by_outgoing_labels(lts, pb.Priority()).block),
+                 "trivial": [0] * n, "discrete": list(range(n)),
+                 "random": list(pb.partition_from_assignment(assignment).block)}
+        res = {}
+        for name, blk in parts.items():
+            p = pb.Partition(blk)
+            q = pb.quotient(lts, p)
+            res[name] = {"block": blk, "stable": ref_is_stable(lts, p),
+                         "q_n": q.n, "q_initial": q.initial_state,
+                         "q_src": [t.source for t in q.transitions],
+                         "q_act": [t.action for t in q.transitions],
+                         "q_dst": [t.target for t in q.transitions]}
+        out.append({"n": n, "num_actions": A, "initial_state": init, "src": rec["src"],
+                    "act": rec["act"], "dst": rec["dst"], "assignment": assignment,
+                    "canonical": res["random"]["block"], "partitions": res})
+    with gzip.open(os.path.join(OUT, "post.json.gz"), "wt") as fh:
+        json.dump(out, fh, separators=(",", ":"))
+    print(f"wrote post.json.gz ({len(out)} instances)")
+
+
+def aut(fuzz=3000):
+    """parse_aut (aut.py:79-92) outcomes of the unmodified reference: the
+    reference's own test texts (tests/test_aut.py:23-64), hand-written edge
+    cases, write_aut round trips of sweep instances with awkward labels, and
+    random single-character mutations of small files (error paths)."""
+    pb = _ref()
+    from parbisim.aut import ParseError, write_aut
+
+    def outcome(text):
+        try:
+            lts = pb.parse_aut(text)
+        except ParseError as e:
+            return {"error": str(e), "line": e.line}
+        return {"n": lts.n, "initial": lts.initial_state, "labels": list(lts.action_labels),
+                "src": [t.source for t in lts.transitions],
+                "act": [t.action for t in lts.transitions],
+                "dst": [t.target for t in lts.transitions]}
+
+    texts = [
+        'des (0,1,2)\n(0,"a",1)', 'des (0,2,2)\n(0,a,1)\n(1,"b c",0)',
+        'des (0,1,2)\n(0,"send(x, y)",1)', "des (0,3,2)\n(0,a,1)", "res (0,1,2)\n(0,a,1)",
+        "des (0,2,2)\n(0,a,1)\n(0,a,2)", 'des (0,1,2)\n(0,"a,1)', "des (2,0,2)\n",
+        "des ( 0 , 1 , 2 )\r\n( 0 , a , 1 )\r\n\r\n", "", "\n", " ", "des (0,0,1)",
+        "des (0,0,0)", "des (0, 0, 1)\n\n\n", "des(0,1,1)\n(0,a,0)", "des (0,1,1) x\n(0,a,0)",
+        "  des (0,1,1)  \n(0,a,0)", "des (0,1,1)\r(0,a,0)", "des (0,1,1)\x0b(0,a,0)",
+        "des (0,1,1)\x0c(0,a,0)\x1c", "des (0,1,1)\x1d(0,a,0)\x1e", "des (0,1,1)\x85(0,a,0)",
+        "des (0,1,1)\u2028(0,a,0)\u2029", "des (0,1,1)\n\x1f(0,a,0)\x1f", "des (0,1,1)\n\xa0(0,a,0)",
+        "des (0,1,1)\n\u3000(0,\u2003a\u2003,0)", "des (0,1,3)\n(+1,a,2)", "des (0,1,3)\n(007,a,0_2)",
+        "des (0,1,3)\n(1_0,a,2)", "des (0,1,3)\n(-1,a,2)", "des (0,1,3)\n(-0,a,2)",
+        "des (0,1,3)\n(1__0,a,2)", "des (0,1,3)\n(_1,a,2)", "des (0,1,3)\n(1_,a,2)",
+        "des (0,1,3)\n(+,a,2)", "des (0,1,3)\n( ,a,2)", "des (0,1,3)\n(0x1,a,2)",
+        "des (0,1,3)\n(99999999999999999999999,a,2)", "des (0,1,3)\n(1,a,99999999999)",
+        "des (0,1,3)\n(1,,2)", "des (0,1,3)\n(1, ,2)", 'des (0,1,3)\n(1,"",2)',
+        'des (0,1,3)\n(1,",2)', 'des (0,1,3)\n(1,"a"b",2)', 'des (0,1,3)\n(1,a"b,2)',
+        "des (0,1,3)\n(1,a(b,2)", "des (0,1,3)\n(1,a)b,2)", "des (0,1,3)\n(1,a,b,2)",
+        'des (0,1,3)\n(1,"a,b",2)', "des (0,1,3)\n(1,a 2)", "des (0,1,3)\n(1 a 2)",
+        "des (0,1,3)\n1,a,2)", "des (0,1,3)\n(1,a,2", "des (0,1,3)\n()", "des (0,1,3)\n(,)",
+        "des (0,1,3)\n(,,)", "des (0,1,3)\n(", "des (0,1,3)\n)", "des (0,1,3)\n(1,a,2) x",
+        "des (0,1,3)\n(x,a,y)", "des (0,1,3)\n(x',a,y)", "des (0,1,3)\n(x'\",a,y)",
+        "des (0,1,3)\n(\\,a,\t)", "des (0,1,3)\n(\x7f,a,\x01)", "des (0,1,3)\n(\xe9,a,\xad)",
+        "des (0,1,3)\n(1,\xe9t\xe9,2)", 'des (0,2,3)\n(1,"z",2)\n(0,"\xe9",1)',
+        'des (0,3,3)\n(1,b,2)\n(0,"B",1)\n(2,"a b",0)', "des (0,2,3)\n(0,a,1)\n(0,a,1)",
+        "des (1,2,3)\n(0,a,1)\n(1,a,2)\n", "des (00,01,03)\n(0,a,1)", "des (0,1,3)\n\n\n(0,a,1)\n\n",
+        "des (0,2,3)\n(0,a,1)", "des (0,0,3)\n(0,a,1)", "des (0,1,3)\n(0,a,1)\n(0,a,1)\n(x)",
+        "des (0,1,3)\n(0,a,5)\n(x)", "des (-1,1,3)\n(0,a,1)", "des (0,1,3,4)\n(0,a,1)",
+        "DES (0,1,3)\n(0,a,1)", "des (0,1,3\n(0,a,1)", "des 0,1,3)\n(0,a,1)",
+        "des (0,99999999999999999999,3)\n(0,a,1)", "des (5,1,99999999999999999999)\n(0,a,1)",
+    ]
+    recs = [{"text": t, "ref": outcome(t)} for t in texts]
+    # write_aut round trips with awkward labels
+    with gzip.open(os.path.join(OUT, "sweep.json.gz"), "rt") as fh:
+        sweep_recs = json.load(fh)[:200]
+    pool = ["a", "b c", "send(x, y)", "\xe9t\xe9", "q\"r", "x,y", "tau", "i", "A", "\u2603"]
+    rng = random.Random(4242)
+    for rec in sweep_recs:
+        A = rec["num_actions"]
+        labels = tuple(sorted(rng.sample(pool, A))) if A <= len(pool) else tuple(
+            f"l{k}" for k in range(A))
+        lts = pb.Lts(n=rec["n"], action_labels=labels,
+                     transitions=tuple(pb.Transition(s, a, t) for s, a, t in
+                                       zip(rec["src"], rec["act"], rec["dst"])),
+                     initial_state=rng.randrange(rec["n"]))
+        t = write_aut(lts)
+        recs.append({"text": t, "ref": outcome(t)})
+    # single-character mutations of small files
+    alphabet = list("0123456789,()\" _-+ab\t\r\n\x0b\x0c\x1c\x85\xa0\xe9\u2028")
+    bases = [r["text"] for r in recs if len(r["text"]) < 400 and "error" not in r["ref"]][:80]
+    for _ in range(fuzz):
+        t = rng.choice(bases)
+        k = rng.randrange(len(t) + 1)
+        op = rng.randrange(3)
+        if op == 0 and k < len(t):
+            t = t[:k] + t[k + 1:]
+        elif op == 1:
+            t = t[:k] + rng.choice(alphabet) + t[k:]
+        elif k < len(t):
+            t = t[:k] + rng.choice(alphabet) + t[k + 1:]
+        recs.append({"text": t, "ref": outcome(t)})
+    with gzip.open(os.path.join(OUT, "aut.json.gz"), "wt", encoding="utf-8") as fh:
+        json.dump(recs, fh, separators=(",", ":"))
+    errs = sum("error" in r["ref"] for r in recs)
+    print(f"wrote aut.json.gz ({len(recs)} texts, {errs} parse errors)")
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     what = sys.argv[1] if len(sys.argv) > 1 else "cases"
-    {"cases": cases, "sweep": sweep, "c1": c1}[what]()
+    {"cases": cases, "sweep": sweep, "c1": c1, "post": post, "aut": aut}[what]()

@@ -51,6 +51,15 @@ class Options(ctypes.Structure):
                 ("observer_user", ctypes.c_void_p)]
 
 
+class AutInfo(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32),
+                ("initial_state", ctypes.c_int32),
+                ("m", ctypes.c_int64),
+                ("num_actions", ctypes.c_int32),
+                ("pad", ctypes.c_int32),
+                ("error_line", ctypes.c_int64)]
+
+
 class NativeError(RuntimeError):
     def __init__(self, code: int, message: str):
         self.code = code
@@ -62,7 +71,9 @@ _lock = threading.Lock()
 
 EXPORTS = ("bisim_bcrp", "bisim_rcpp", "bisim_bcrp_ex", "bisim_rcpp_ex", "bisim_bcrp_device",
            "bisim_rcpp_device", "bisim_preprocess", "bisim_label_partition", "bisim_last_error",
-           "bisim_device_count", "bisim_stream", "bisim_version")
+           "bisim_device_count", "bisim_stream", "bisim_version", "bisim_quotient",
+           "bisim_is_stable", "bisim_canonical", "bisim_aut_parse", "bisim_aut_read_file",
+           "bisim_aut_columns", "bisim_aut_label", "bisim_aut_free")
 
 
 def lib():
@@ -94,9 +105,24 @@ def lib():
             L.bisim_preprocess.argtypes = [i32, i64, i32, i32p, i32p, i32p, i32p, i32p, P(i64),
                                            ctypes.c_int]
             L.bisim_label_partition.argtypes = [i32, i64, i32, i32p, i32p, i32p, ctypes.c_int]
+            L.bisim_quotient.argtypes = [i32, i64, i32, i32p, i32p, i32p, i32p, i32, P(i32),
+                                         P(i64), i32p, i32p, i32p, P(i32), ctypes.c_int]
+            L.bisim_is_stable.argtypes = [i32, i64, i32, i32p, i32p, i32p, i32p, P(i32),
+                                          ctypes.c_int]
+            L.bisim_canonical.argtypes = [i32, P(i64), i32p, ctypes.c_int]
+            vp = ctypes.c_void_p
+            L.bisim_aut_parse.argtypes = [ctypes.c_char_p, i64, i32, P(vp), P(AutInfo)]
+            L.bisim_aut_read_file.argtypes = [ctypes.c_char_p, i32, P(vp), P(AutInfo)]
+            L.bisim_aut_columns.argtypes = [vp, i32p, i32p, i32p]
+            L.bisim_aut_label.argtypes = [vp, i32, P(i64)]
+            L.bisim_aut_label.restype = vp
+            L.bisim_aut_free.argtypes = [vp]
+            L.bisim_aut_free.restype = None
             for name in ("bisim_bcrp", "bisim_rcpp", "bisim_bcrp_ex", "bisim_rcpp_ex",
                          "bisim_bcrp_device", "bisim_rcpp_device", "bisim_preprocess",
-                         "bisim_label_partition", "bisim_device_count"):
+                         "bisim_label_partition", "bisim_device_count", "bisim_quotient",
+                         "bisim_is_stable", "bisim_canonical", "bisim_aut_parse", "bisim_aut_read_file",
+           "bisim_aut_columns", "bisim_aut_label", "bisim_aut_free"):
                 getattr(L, name).restype = ctypes.c_int
             L.bisim_last_error.restype = ctypes.c_char_p
             L.bisim_last_error.argtypes = []

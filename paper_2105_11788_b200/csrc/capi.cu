@@ -614,6 +614,11 @@ bisim_options opts_or_default(const bisim_options* o, int device) {
 }  // namespace
 }  // namespace bisim
 
+namespace bisim {
+// used by aut.cpp (host-only translation unit)
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace bisim
+
 using namespace bisim;
 
 extern "C" {
@@ -828,3 +833,5 @@ void* bisim_stream(int device) {
 const char* bisim_version(void) { return "libbisim 0.1 (sm_100a, dense persistent loop)"; }
 
 }  // extern "C"
+
+#include "post.cuh"
