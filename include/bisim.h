@@ -123,6 +123,25 @@ int bisim_rcpp_device(int32_t n, int64_t m, const int32_t *d_src, const int32_t 
                       int32_t *splits_out, int64_t splits_cap, bisim_stats *st,
                       const bisim_options *opt);
 
+/* ---- transition-sharded mode ----------------------------- */
+/* One LTS refined by nshards replicas on devices[0..nshards) (1..8; a
+ * device may repeat, which runs several replicas on one GPU for testing).
+ * Every replica keeps the whole partition state; the in-edges are split by
+ * source range (about m / nshards each) and every round's marks are OR-ed
+ * into all replicas over peer memory inside the persistent kernels, with one
+ * cross-replica barrier per round.  Same results and RunStats as bisim_bcrp /
+ * bisim_rcpp (host pointers; no observer).  flags: BISIM_SHARD_VERIFY also
+ * checks that every replica ends with the same partition. */
+#define BISIM_SHARD_VERIFY 1
+int bisim_bcrp_sharded(int32_t n, int64_t m, int32_t num_actions, const int32_t *src,
+                       const int32_t *act, const int32_t *dst, int64_t max_supersteps,
+                       int32_t *block_out, int32_t *splits_out, int64_t splits_cap,
+                       bisim_stats *st, const int32_t *devices, int32_t nshards, int32_t flags);
+int bisim_rcpp_sharded(int32_t n, int64_t m, const int32_t *src, const int32_t *dst,
+                       const int32_t *pi0_leader, int64_t max_supersteps, int32_t *block_out,
+                       int32_t *splits_out, int64_t splits_cap, bisim_stats *st,
+                       const int32_t *devices, int32_t nshards, int32_t flags);
+
 /* ---- preprocessing tables (bcrp.py:116-126, BcrpAux) -------------------- */
 /* Per ORIGINAL transition index i: order_out[i] = rank of act[i] among
  * src[i]'s distinct labels; per state: nr_marks_out[s], off_out[s].  Returns

@@ -16,6 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libbisim.so")
 
 BISIM_OK, BISIM_BAD_INPUT, BISIM_GUARD, BISIM_CUDA, BISIM_ABORTED = 0, 1, 2, 3, 4
+SHARD_VERIFY = 1
 DEFAULT_GUARD = -(2 ** 63)
 MODE_AUTO, MODE_PERSISTENT, MODE_STEPPED, MODE_DENSE = 0, 1, 2, 3
 
@@ -73,7 +74,8 @@ EXPORTS = ("bisim_bcrp", "bisim_rcpp", "bisim_bcrp_ex", "bisim_rcpp_ex", "bisim_
            "bisim_rcpp_device", "bisim_preprocess", "bisim_label_partition", "bisim_last_error",
            "bisim_device_count", "bisim_stream", "bisim_version", "bisim_quotient",
            "bisim_is_stable", "bisim_canonical", "bisim_aut_parse", "bisim_aut_read_file",
-           "bisim_aut_columns", "bisim_aut_label", "bisim_aut_free")
+           "bisim_aut_columns", "bisim_aut_label", "bisim_aut_free", "bisim_bcrp_sharded",
+           "bisim_rcpp_sharded")
 
 
 def lib():
@@ -110,6 +112,10 @@ def lib():
             L.bisim_is_stable.argtypes = [i32, i64, i32, i32p, i32p, i32p, i32p, P(i32),
                                           ctypes.c_int]
             L.bisim_canonical.argtypes = [i32, P(i64), i32p, ctypes.c_int]
+            L.bisim_bcrp_sharded.argtypes = [i32, i64, i32, i32p, i32p, i32p, i64, i32p, i32p, i64,
+                                             P(Stats), i32p, i32, i32]
+            L.bisim_rcpp_sharded.argtypes = [i32, i64, i32p, i32p, i32p, i64, i32p, i32p, i64,
+                                             P(Stats), i32p, i32, i32]
             vp = ctypes.c_void_p
             L.bisim_aut_parse.argtypes = [ctypes.c_char_p, i64, i32, P(vp), P(AutInfo)]
             L.bisim_aut_read_file.argtypes = [ctypes.c_char_p, i32, P(vp), P(AutInfo)]
@@ -122,7 +128,8 @@ def lib():
                          "bisim_bcrp_device", "bisim_rcpp_device", "bisim_preprocess",
                          "bisim_label_partition", "bisim_device_count", "bisim_quotient",
                          "bisim_is_stable", "bisim_canonical", "bisim_aut_parse", "bisim_aut_read_file",
-           "bisim_aut_columns", "bisim_aut_label", "bisim_aut_free"):
+           "bisim_aut_columns", "bisim_aut_label", "bisim_aut_free", "bisim_bcrp_sharded",
+           "bisim_rcpp_sharded"):
                 getattr(L, name).restype = ctypes.c_int
             L.bisim_last_error.restype = ctypes.c_char_p
             L.bisim_last_error.argtypes = []

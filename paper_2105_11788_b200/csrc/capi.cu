@@ -84,6 +84,8 @@ int occupancy_grid(const void* fn, int sms, int threads = kThreads, int max_per_
     return sms * std::min(occ, max_per_sm);
 }
 
+std::unique_ptr<Ctx> make_ctx(int device);
+
 Ctx* get_ctx(int device) {
     std::lock_guard<std::mutex> g(g_ctx_mu);
     int count = 0;
@@ -91,7 +93,12 @@ Ctx* get_ctx(int device) {
         throw Error(BISIM_CUDA, "no CUDA device available (libbisim has no CPU fallback)");
     if (device < 0 || device >= count) throw Error(BISIM_CUDA, "invalid CUDA device ordinal");
     if ((int)g_ctx.size() < count) g_ctx.resize(count);
-    if (!g_ctx[device]) {
+    if (!g_ctx[device]) g_ctx[device] = make_ctx(device);
+    return g_ctx[device].get();
+}
+
+std::unique_ptr<Ctx> make_ctx(int device) {
+    {
         auto c = std::make_unique<Ctx>();
         c->device = device;
         CK(cudaSetDevice(device));
@@ -104,11 +111,10 @@ Ctx* get_ctx(int device) {
         c->grid_refine_bcrp = occupancy_grid((const void*)k_refine<false>, c->sms);
         c->grid_refine_rcpp = occupancy_grid((const void*)k_refine<true>, c->sms);
         c->grid_label = occupancy_grid((const void*)k_label_rounds, c->sms);
-        c->grid_sparse_bcrp = occupancy_grid((const void*)k_refine_sparse<false>, c->sms, kSparseThreads, 1);
-        c->grid_sparse_rcpp = occupancy_grid((const void*)k_refine_sparse<true>, c->sms, kSparseThreads, 1);
-        g_ctx[device] = std::move(c);
+        c->grid_sparse_bcrp = occupancy_grid((const void*)k_refine_sparse<false, false>, c->sms, kSparseThreads, 1);
+        c->grid_sparse_rcpp = occupancy_grid((const void*)k_refine_sparse<true, false>, c->sms, kSparseThreads, 1);
+        return c;
     }
-    return g_ctx[device].get();
 }
 
 int grid_for(int64_t work, int threads, int sms) {
@@ -141,6 +147,23 @@ struct Job {
     int64_t splits_cap = 0;
     bisim_stats* st = nullptr;
     bisim_options opt{};
+    // transition-sharded mode (sharded.cuh): reverse CSR over sources in
+    // [src_lo, src_hi) only, double-buffered round state, and run() stops
+    // after the setup, handing the loop parameters to the caller
+    int32_t src_lo = 0, src_hi = -1;
+    struct ShardPrep* prep = nullptr;
+};
+
+// What run() leaves for the sharded driver when Job::prep is set.
+struct ShardPrep {
+    SparseParams sp{};
+    bisim_stats S{};
+    int64_t guard = 0;
+    int64_t splits_dev_cap = 0;
+    int32_t* block = nullptr;
+    int32_t* splits = nullptr;
+    int32_t* leaders = nullptr;
+    int64_t mark_words = 0, bm_words = 0;
 };
 
 template <typename T>
@@ -181,7 +204,11 @@ int64_t loop_bytes(bool bcrp, bool dense, int32_t n, int64_t L, int64_t R, const
     return (R + 1) * 64 + (int64_t)ls.work_edges * per_edge + (int64_t)ls.work_members * per_member;
 }
 
-int run(Job& j) {
+int run_with(Ctx& c, Job& j);
+
+int run(Job& j) { return run_with(*get_ctx(j.opt.device), j); }
+
+int run_with(Ctx& c, Job& j) {
     if (j.n < 1) throw Error(BISIM_BAD_INPUT, "state count must be at least 1");
     if (j.m < 0 || j.m >= (int64_t)INT32_MAX) throw Error(BISIM_BAD_INPUT, "transition count out of range");
     if (j.A < 0) throw Error(BISIM_BAD_INPUT, "negative action count");
@@ -191,7 +218,6 @@ int run(Job& j) {
     if (!j.bcrp && !j.pi0) throw Error(BISIM_BAD_INPUT, "null pi0");
     if (!j.block_out) throw Error(BISIM_BAD_INPUT, "null block_out");
 
-    Ctx& c = *get_ctx(j.opt.device);
     std::lock_guard<std::mutex> lock(c.mu);
     CK(cudaSetDevice(c.device));
     c.launches = 0;
@@ -203,8 +229,10 @@ int run(Job& j) {
     const int64_t guard = j.max_supersteps == BISIM_DEFAULT_GUARD
                               ? (j.bcrp ? 3LL * n + A + 8 : 3LL * n + 9)
                               : j.max_supersteps;
-    const bool stepped = j.opt.observer != nullptr || j.opt.mode == BISIM_MODE_STEPPED;
-    const bool dense = j.opt.mode == BISIM_MODE_DENSE;
+    const bool sharded = j.prep != nullptr;
+    const bool stepped = !sharded && (j.opt.observer != nullptr || j.opt.mode == BISIM_MODE_STEPPED);
+    const bool dense = !sharded && j.opt.mode == BISIM_MODE_DENSE;
+    const int32_t src_lo = sharded ? j.src_lo : 0, src_hi = sharded ? j.src_hi : n;
     bisim_stats S{};
     S.label_rounds = A;
     S.mode = stepped ? BISIM_MODE_STEPPED : (dense ? BISIM_MODE_DENSE : BISIM_MODE_PERSISTENT);
@@ -248,7 +276,8 @@ int run(Job& j) {
     int32_t* block = (int32_t*)c.block.ensure((int64_t)n * 4);
     const int64_t mark_bits = j.bcrp ? m : n;  // L <= m (bcrp.py:113)
     const int64_t mark_words = (mark_bits + 31) / 32 + 2;
-    uint32_t* mark = (uint32_t*)c.mark.ensure(mark_words * 4);
+    const int parities = sharded ? 2 : 1;  // sharded: one buffer per round parity
+    uint32_t* mark = (uint32_t*)c.mark.ensure(parities * mark_words * 4);
     const int64_t nwords = ((int64_t)n + 31) / 32;
     // rounds can never exceed the guard nor the 3n bound of the paper
     const int64_t splits_dev_cap =
@@ -277,7 +306,8 @@ int run(Job& j) {
     }
     CK(cudaMemsetAsync(rev_ptr, 0, ((int64_t)n + 1) * 4, st));
     if (m) {
-        k_indeg<<<grid_for(m, TB, c.sms), TB, 0, st>>>(m, d_dst, rev_ptr);
+        k_indeg<<<grid_for(m, TB, c.sms), TB, 0, st>>>(m, d_dst, rev_ptr, sharded ? d_src : nullptr, src_lo,
+                                                       src_hi);
         ++c.launches;
     }
     scan_excl(c, rev_ptr, n);
@@ -295,9 +325,11 @@ int run(Job& j) {
         else if (dense)
             k_rev_fill<false><<<g, TB, 0, st>>>(n, m, d_src, d_act, d_dst, lmask, off, cursor, rev_slot);
         else if (j.bcrp)
-            k_rev_fill2<true><<<g, TB, 0, st>>>(n, m, d_src, d_act, d_dst, lmask, off, cursor, rev2, nullptr);
+            k_rev_fill2<true><<<g, TB, 0, st>>>(n, m, d_src, d_act, d_dst, lmask, off, cursor, rev2, nullptr,
+                                                src_lo, src_hi);
         else
-            k_rev_fill2<false><<<g, TB, 0, st>>>(n, m, d_src, d_act, d_dst, lmask, off, cursor, nullptr, rev_src);
+            k_rev_fill2<false><<<g, TB, 0, st>>>(n, m, d_src, d_act, d_dst, lmask, off, cursor, nullptr, rev_src,
+                                                 src_lo, src_hi);
         ++c.launches;
     }
     CK(cudaGetLastError());
@@ -366,7 +398,7 @@ int run(Job& j) {
     k_count_leaders<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, block, leaders);
     c.launches += 2;
     CK(cudaMemcpyAsync(&h_leaders, leaders, 4, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemsetAsync(mark, 0, mark_words * 4, st));
+    CK(cudaMemsetAsync(mark, 0, parities * mark_words * 4, st));
     CK(cudaMemsetAsync(splits, 0, splits_dev_cap * 4, st));
 
     // ---- loop state
@@ -416,10 +448,10 @@ int run(Job& j) {
         k_summary<<<grid_for((int64_t)nw1 * 32, TB, c.sms), TB, 0, st>>>(U, nw0, U1, nw1);
         k_summary<<<1, 64, 0, st>>>(U1, nw1, U2, nw2);
         c.launches += 2;
-        uint32_t* touched = (uint32_t*)c.touched.ensure((nwords + 2) * 4);
-        uint32_t* tblock = (uint32_t*)c.tblock.ensure((nwords + 2) * 4);
-        CK(cudaMemsetAsync(touched, 0, (nwords + 2) * 4, st));
-        CK(cudaMemsetAsync(tblock, 0, (nwords + 2) * 4, st));
+        uint32_t* touched = (uint32_t*)c.touched.ensure(parities * (nwords + 2) * 4);
+        uint32_t* tblock = (uint32_t*)c.tblock.ensure(parities * (nwords + 2) * 4);
+        CK(cudaMemsetAsync(touched, 0, parities * (nwords + 2) * 4, st));
+        CK(cudaMemsetAsync(tblock, 0, parities * (nwords + 2) * 4, st));
         sp.n = n;
         sp.A = A;
         sp.reflag_c = j.bcrp ? 1 : 0;
@@ -473,6 +505,27 @@ int run(Job& j) {
     CK(cudaEventRecord(c.ev[3], st));
     CK(cudaStreamSynchronize(st));
     S.initial_blocks = h_leaders;
+    if (sharded) {
+        ShardPrep& P = *j.prep;
+        sp.mark_stride = mark_words;
+        sp.bm_stride = nwords + 2;
+        sp.allow_skip = 0;  // skip steps read in-edges of other shards
+        sp.allow_solo = 0;
+        P.sp = sp;
+        P.S = S;
+        P.guard = guard;
+        P.splits_dev_cap = splits_dev_cap;
+        P.block = block;
+        P.splits = splits;
+        P.leaders = leaders;
+        P.mark_words = mark_words;
+        P.bm_words = nwords + 2;
+        S.t_h2d_ms = elapsed(c.ev[0], c.ev[1]);
+        S.t_pre_ms = elapsed(c.ev[1], c.ev[2]);
+        S.t_label_ms = elapsed(c.ev[2], c.ev[3]);
+        P.S = S;
+        return BISIM_OK;
+    }
 
     // ---- refinement loop
     const void* kfn;
@@ -483,7 +536,7 @@ int run(Job& j) {
         kgrid = j.bcrp ? c.grid_refine_bcrp : c.grid_refine_rcpp;
         kargs[0] = &lp;
     } else {
-        kfn = j.bcrp ? (const void*)k_refine_sparse<false> : (const void*)k_refine_sparse<true>;
+        kfn = j.bcrp ? (const void*)k_refine_sparse<false, false> : (const void*)k_refine_sparse<true, false>;
         kgrid = j.bcrp ? c.grid_sparse_bcrp : c.grid_sparse_rcpp;
         kthreads = kSparseThreads;
         kargs[0] = &sp;
@@ -589,12 +642,242 @@ int run(Job& j) {
     return BISIM_OK;
 }
 
+// ---- transition-sharded mode (kernels_shard.cuh) ------------------------------
+
+// Per-shard resources, cached across calls with the same device list.
+struct ShardSet {
+    std::vector<int32_t> devices;
+    std::vector<std::unique_ptr<Ctx>> ctx;
+    std::vector<DevBuf> xlist, xcnt, xbar, go;
+};
+std::mutex g_shard_mu;
+std::unique_ptr<ShardSet> g_shards;
+
+ShardSet& shard_set(const int32_t* devices, int G) {
+    std::vector<int32_t> want(devices, devices + G);
+    if (!g_shards || g_shards->devices != want) {
+        int count = 0;
+        if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+            throw Error(BISIM_CUDA, "no CUDA device available (libbisim has no CPU fallback)");
+        auto S = std::make_unique<ShardSet>();
+        S->devices = want;
+        for (int g = 0; g < G; ++g) {
+            if (want[g] < 0 || want[g] >= count) throw Error(BISIM_CUDA, "invalid CUDA device ordinal");
+            S->ctx.push_back(make_ctx(want[g]));
+        }
+        S->xlist.resize(G);
+        S->xcnt.resize(G);
+        S->xbar.resize(G);
+        S->go.resize(G);
+        // peer access between distinct devices (NVLink / NVSwitch)
+        for (int a = 0; a < G; ++a)
+            for (int b = 0; b < G; ++b) {
+                if (want[a] == want[b]) continue;
+                int ok = 0;
+                CK(cudaDeviceCanAccessPeer(&ok, want[a], want[b]));
+                if (!ok) throw Error(BISIM_CUDA, "devices cannot access each other's memory (no P2P)");
+                CK(cudaSetDevice(want[a]));
+                const cudaError_t e = cudaDeviceEnablePeerAccess(want[b], 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+                cudaGetLastError();
+            }
+        g_shards = std::move(S);
+    }
+    return *g_shards;
+}
+
+// Source ranges with about m / G transitions each (out-degree prefix sums on
+// the first shard's device).
+std::vector<int32_t> shard_bounds(Ctx& c, int32_t n, int64_t m, const int32_t* d_src, int G) {
+    std::vector<int32_t> lo(G + 1, n);
+    lo[0] = 0;
+    if (m == 0) {
+        for (int g = 1; g < G; ++g) lo[g] = (int32_t)((int64_t)n * g / G);
+        return lo;
+    }
+    int32_t* deg = (int32_t*)c.cursor.ensure(((int64_t)n + 1) * 4);
+    CK(cudaMemsetAsync(deg, 0, ((int64_t)n + 1) * 4, c.stream));
+    k_indeg<<<grid_for(m, 256, c.sms), 256, 0, c.stream>>>(m, d_src, deg);
+    scan_excl(c, deg, n);
+    int32_t* dlo = (int32_t*)c.counter.ensure(4 * (kMaxShards + 2));
+    k_shard_cuts<<<1, 32, 0, c.stream>>>(deg, n, G, dlo);
+    CK(cudaMemcpyAsync(lo.data(), dlo, 4 * (G + 1), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    return lo;
+}
+
+int run_sharded(Job& base, const int32_t* devices, int G, int32_t flags) {
+    if (G < 1 || G > kMaxShards) throw Error(BISIM_BAD_INPUT, "shard count must be 1..8");
+    if (!devices) throw Error(BISIM_BAD_INPUT, "null device list");
+    if (base.n < 1) throw Error(BISIM_BAD_INPUT, "state count must be at least 1");
+    std::lock_guard<std::mutex> lock(g_shard_mu);
+    ShardSet& S = shard_set(devices, G);
+    const int32_t n = base.n;
+    const int64_t m = base.m;
+    // shard bounds: copy src to shard 0 once to find them
+    Ctx& c0 = *S.ctx[0];
+    CK(cudaSetDevice(c0.device));
+    std::vector<int32_t> lo;
+    {
+        const int64_t mm = std::max<int64_t>(m, 1);
+        int32_t* d_src = (int32_t*)c0.src.ensure(mm * 4);
+        if (m) CK(cudaMemcpyAsync(d_src, base.src, m * 4, cudaMemcpyHostToDevice, c0.stream));
+        lo = shard_bounds(c0, n, m, d_src, G);
+    }
+    // every replica: inputs, preprocessing, label partition, loop state
+    std::vector<ShardPrep> prep(G);
+    for (int g = 0; g < G; ++g) {
+        Ctx& c = *S.ctx[g];
+        Job j = base;
+        j.prep = &prep[g];
+        j.src_lo = lo[g];
+        j.src_hi = lo[g + 1];
+        j.opt.device = c.device;
+        bisim_stats st{};
+        j.st = &st;
+        run_with(c, j);
+    }
+    for (int g = 0; g < G; ++g) {
+        Ctx& c = *S.ctx[g];
+        CK(cudaSetDevice(c.device));
+        int32_t* xl = (int32_t*)S.xlist[g].ensure(2 * (int64_t)n * 4);
+        (void)xl;
+        CK(cudaMemsetAsync(S.xcnt[g].ensure(16), 0, 16, c.stream));
+        CK(cudaMemsetAsync(S.xbar[g].ensure(128), 0, 128, c.stream));
+        CK(cudaMemsetAsync(S.go[g].ensure(128), 0, 128, c.stream));
+        CK(cudaMemsetAsync(prep[g].sp.bar, 0, sizeof(GridBarrier), c.stream));
+    }
+    for (int g = 0; g < G; ++g) {
+        SparseParams& sp = prep[g].sp;
+        sp.nshard = G;
+        sp.shard = g;
+        sp.xlist = (int32_t*)S.xlist[g].p;
+        sp.go = (unsigned*)S.go[g].p;
+        sp.timeout_ns = 20ull * 1000 * 1000 * 1000;
+        for (int r = 0; r < G; ++r) {
+            sp.peer_mark[r] = prep[r].sp.mark;
+            sp.peer_touched[r] = prep[r].sp.touched;
+            sp.peer_xlist[r] = (int32_t*)S.xlist[r].p;
+            sp.peer_xcnt[r] = (int32_t*)S.xcnt[r].p;
+            sp.peer_xbar[r] = (unsigned*)S.xbar[r].p;
+        }
+    }
+    for (int g = 0; g < G; ++g) CK(cudaStreamSynchronize(S.ctx[g]->stream));
+    // launch every replica; a device holding several replicas (testing on
+    // one GPU) splits its SMs between them and uses plain launches
+    std::vector<cudaEvent_t> t0(G), t1(G);
+    for (int g = 0; g < G; ++g) {
+        Ctx& c = *S.ctx[g];
+        CK(cudaSetDevice(c.device));
+        const int same = (int)std::count(S.devices.begin(), S.devices.end(), c.device);
+        const void* kfn = base.bcrp ? (const void*)k_refine_sparse<false, true> : (const void*)k_refine_sparse<true, true>;
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kSparseThreads, 0));
+        if (occ < 1) throw Error(BISIM_CUDA, "sharded kernel cannot be resident");
+        t0[g] = c.ev[3];
+        t1[g] = c.ev[4];
+        CK(cudaEventRecord(t0[g], c.stream));
+        void* args[] = {&prep[g].sp};
+        if (same == 1) {
+            CK(cudaLaunchCooperativeKernel(kfn, c.sms, kSparseThreads, args, 0, c.stream));
+        } else {
+            const int grid = std::max(1, c.sms / same);
+            CK(cudaLaunchKernel(kfn, grid, kSparseThreads, args, 0, c.stream));
+        }
+        CK(cudaEventRecord(t1[g], c.stream));
+        ++c.launches;
+    }
+    std::vector<SCtrl> hc(G);
+    for (int g = 0; g < G; ++g) {
+        Ctx& c = *S.ctx[g];
+        CK(cudaSetDevice(c.device));
+        CK(cudaMemcpyAsync(&hc[g], prep[g].sp.ctrl, sizeof(SCtrl), cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaStreamSynchronize(c.stream));
+    }
+    for (int g = 0; g < G; ++g) {
+        if (hc[g].error == kShardTimeout)
+            throw Error(BISIM_CUDA, "sharded replicas did not run concurrently (cross-replica wait timed out)");
+        if (hc[g].round != hc[0].round || hc[g].error != hc[0].error)
+            throw Error(BISIM_CUDA, "sharded replicas diverged");
+    }
+    ShardPrep& P = prep[0];
+    bisim_stats St = P.S;
+    St.supersteps = hc[0].round;
+    St.mode = BISIM_MODE_PERSISTENT;
+    if (hc[0].error == BISIM_GUARD) {
+        St.guard_count = hc[0].guard_count;
+        if (base.st) *base.st = St;
+        throw Error(BISIM_GUARD, "superstep guard exceeded (" + std::to_string(hc[0].guard_count) + " > " +
+                                     std::to_string(P.guard) + ")");
+    }
+    float alg = 0.f;
+    for (int g = 0; g < G; ++g) {
+        CK(cudaSetDevice(S.ctx[g]->device));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, t0[g], t1[g]));
+        alg = std::max(alg, ms);
+    }
+    // results from replica 0 (optionally checked against every replica)
+    CK(cudaSetDevice(c0.device));
+    CK(cudaMemsetAsync(P.leaders, 0, 4, c0.stream));
+    k_count_leaders<<<grid_for(n, 256, c0.sms), 256, 0, c0.stream>>>(n, P.block, P.leaders);
+    CK(cudaMemcpyAsync(base.block_out, P.block, (int64_t)n * 4, cudaMemcpyDeviceToHost, c0.stream));
+    const int64_t R = hc[0].round;
+    const int64_t ncopy = std::min<int64_t>(std::min<int64_t>(R, base.splits_cap), P.splits_dev_cap);
+    if (base.splits_out && ncopy > 0)
+        CK(cudaMemcpyAsync(base.splits_out, P.splits, ncopy * 4, cudaMemcpyDeviceToHost, c0.stream));
+    int32_t fin = 0;
+    CK(cudaMemcpyAsync(&fin, P.leaders, 4, cudaMemcpyDeviceToHost, c0.stream));
+    CK(cudaStreamSynchronize(c0.stream));
+    if (flags & BISIM_SHARD_VERIFY) {
+        std::vector<int32_t> other(n);
+        for (int g = 1; g < G; ++g) {
+            CK(cudaSetDevice(S.ctx[g]->device));
+            CK(cudaMemcpy(other.data(), prep[g].block, (int64_t)n * 4, cudaMemcpyDeviceToHost));
+            if (memcmp(other.data(), base.block_out, (size_t)n * 4) != 0)
+                throw Error(BISIM_CUDA, "sharded replicas hold different partitions");
+        }
+    }
+    St.final_blocks = fin;
+    St.t_alg_ms = alg;
+    LoopStatus ls;
+    for (int g = 0; g < G; ++g) {
+        ls.work_edges += hc[g].work_edges;
+        ls.work_members = std::max(ls.work_members, hc[g].work_members);
+    }
+    ls.round = R;
+    St.bytes_alg = loop_bytes(base.bcrp, false, n, St.mark_length, R, ls);
+    St.kernel_launches = G;
+    if (base.st) *base.st = St;
+    return BISIM_OK;
+}
+
 int guarded(Job& j) {
     bisim_stats dummy{};
     if (!j.st) j.st = &dummy;
     try {
         g_last_error.clear();
         return run(j);
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return BISIM_CUDA;
+    }
+}
+
+int sharded_guarded(Job& j, const int32_t* devices, int G, int32_t flags) {
+    bisim_stats dummy{};
+    if (!j.st) j.st = &dummy;
+    try {
+        g_last_error.clear();
+        if (j.n < 1) throw Error(BISIM_BAD_INPUT, "state count must be at least 1");
+        if (j.m < 0 || j.m >= (int64_t)INT32_MAX) throw Error(BISIM_BAD_INPUT, "transition count out of range");
+        if (j.m > 0 && (!j.src || !j.dst || (j.bcrp && !j.act)))
+            throw Error(BISIM_BAD_INPUT, "null transition array");
+        if (!j.block_out) throw Error(BISIM_BAD_INPUT, "null block_out");
+        return run_sharded(j, devices, G, flags);
     } catch (const Error& e) {
         g_last_error = e.what();
         return e.code;
@@ -721,6 +1004,44 @@ int bisim_rcpp_device(int32_t n, int64_t m, const int32_t* d_src, const int32_t*
     j.st = st;
     j.opt = opts_or_default(opt, 0);
     return guarded(j);
+}
+
+int bisim_bcrp_sharded(int32_t n, int64_t m, int32_t num_actions, const int32_t* src, const int32_t* act,
+                       const int32_t* dst, int64_t max_supersteps, int32_t* block_out, int32_t* splits_out,
+                       int64_t splits_cap, bisim_stats* st, const int32_t* devices, int32_t nshards,
+                       int32_t flags) {
+    Job j;
+    j.bcrp = true;
+    j.n = n;
+    j.m = m;
+    j.A = num_actions;
+    j.src = src;
+    j.act = act;
+    j.dst = dst;
+    j.max_supersteps = max_supersteps;
+    j.block_out = block_out;
+    j.splits_out = splits_out;
+    j.splits_cap = splits_cap;
+    j.st = st;
+    return sharded_guarded(j, devices, nshards, flags);
+}
+
+int bisim_rcpp_sharded(int32_t n, int64_t m, const int32_t* src, const int32_t* dst, const int32_t* pi0_leader,
+                       int64_t max_supersteps, int32_t* block_out, int32_t* splits_out, int64_t splits_cap,
+                       bisim_stats* st, const int32_t* devices, int32_t nshards, int32_t flags) {
+    Job j;
+    j.bcrp = false;
+    j.n = n;
+    j.m = m;
+    j.src = src;
+    j.dst = dst;
+    j.pi0 = pi0_leader;
+    j.max_supersteps = max_supersteps;
+    j.block_out = block_out;
+    j.splits_out = splits_out;
+    j.splits_cap = splits_cap;
+    j.st = st;
+    return sharded_guarded(j, devices, nshards, flags);
 }
 
 int bisim_preprocess(int32_t n, int64_t m, int32_t num_actions, const int32_t* src, const int32_t* act,

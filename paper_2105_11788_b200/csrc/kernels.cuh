@@ -68,6 +68,20 @@ __device__ __forceinline__ unsigned long long elect_key(int64_t epoch, int32_t s
 __device__ __forceinline__ int32_t elect_winner(unsigned long long key) {
     return kBig - (int32_t)(unsigned)(key & 0xffffffffull);
 }
+// Fire-and-forget reductions (REDG): unlike atomicOr/And/Min with an unused
+// result, which compile to returning ATOMG, these never hold a scoreboard.
+__device__ __forceinline__ void red_or(uint32_t* a, uint32_t v) {
+    asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_and(uint32_t* a, uint32_t v) {
+    asm volatile("red.relaxed.gpu.global.and.b32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_min(int32_t* a, int32_t v) {
+    asm volatile("red.relaxed.gpu.global.min.s32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_add(int32_t* a, int32_t v) {
+    asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
 __device__ __forceinline__ void set_bit(uint32_t* bm, int32_t i) {
     atomicOr(&bm[i >> 5], 1u << (i & 31));
 }
@@ -218,14 +232,22 @@ __global__ void k_order(int32_t n, int64_t m, const int32_t* __restrict__ src,
 }
 
 // in-degree histogram, warp-aggregated on equal targets
-__global__ void k_indeg(int64_t m, const int32_t* __restrict__ dst, int32_t* cnt) {
+// In-degrees; with src != nullptr only transitions whose source lies in
+// [lo, hi) count (one shard of the transition-sharded mode).
+__global__ void k_indeg(int64_t m, const int32_t* __restrict__ dst, int32_t* cnt,
+                        const int32_t* __restrict__ src = nullptr, int32_t lo = 0, int32_t hi = 0) {
     const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < m; i0 += stride) {
         const int64_t i = i0 + lane;
-        const int32_t t = i < m ? dst[i] : -1 - lane;
+        bool in = i < m;
+        if (in && src) {
+            const int32_t s = src[i];
+            in = s >= lo && s < hi;
+        }
+        const int32_t t = in ? dst[i] : -1 - lane;
         const LaneRun r = lane_run(t);
-        if (i < m && r.rank == 0) atomicAdd(&cnt[t], r.len);
+        if (in && r.rank == 0) atomicAdd(&cnt[t], r.len);
     }
 }
 

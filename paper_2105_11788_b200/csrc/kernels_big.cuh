@@ -207,8 +207,8 @@ __device__ int32_t big_tag(const SparseParams& p, int32_t nbig, int32_t ci) {
     int32_t nsplit, nkeep, wmin;
     chunk_counts<K>(c, bal, kb, nsplit, nkeep, wmin);
     if (lane == 0 && nsplit) {
-        atomicAdd(&p.scnt[l], nsplit);
-        atomicMin(&p.smin[l], wmin);
+        red_add(&p.scnt[l], nsplit);
+        red_min(&p.smin[l], wmin);
     }
     return min(32 * K, bz - ci0);
 }
@@ -251,7 +251,7 @@ __device__ void big_split(const SparseParams& p, int cur, int64_t round, int32_t
         const bool tu = (tw[j] >> (c.r[j].x & 31)) & 1u;
         clear_member<IDENT>(p, c.r[j].x, tu, slot_base<IDENT>(c.r[j]), nrl);
     }
-    if (ci0 == 0 && lane == 0) atomicAnd(&p.tblock[l >> 5], ~(1u << (l & 31)));
+    if (ci0 == 0 && lane == 0) red_and(&p.tblock[l >> 5], ~(1u << (l & 31)));
 }
 
 // one pass (every item on its own warp)
@@ -273,8 +273,8 @@ __device__ int32_t big_onepass(const SparseParams& p, int cur, int64_t round, in
     if (nch_b > 1) {
         if (lane == 0) {
             if (nsplit) {
-                atomicAdd(&p.scnt[l], nsplit);
-                atomicMin(&p.smin[l], wmin);
+                red_add(&p.scnt[l], nsplit);
+                red_min(&p.smin[l], wmin);
             }
             // release: the count/minimum above are visible before the arrival
             asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(&p.sarr[l]) : "memory");
@@ -295,6 +295,142 @@ __device__ int32_t big_onepass(const SparseParams& p, int cur, int64_t round, in
 #pragma unroll
     for (int j = 0; j < K; ++j)
         if (c.valid[j]) clear_member<IDENT>(p, c.r[j].x, c.tu[j], slot_base<IDENT>(c.r[j]), nrl);
-    if (ci0 == 0 && lane == 0) atomicAnd(&p.tblock[l >> 5], ~(1u << (l & 31)));
+    if (ci0 == 0 && lane == 0) red_and(&p.tblock[l >> 5], ~(1u << (l & 31)));
     return min(32 * K, bz - ci0);
 }
+
+// ---- one pass with CTA-level aggregation ----------------------------------
+//
+// Every warp of the CTA calls this once per round (ci < 0: no big chunk).
+// The chunks of one big block that land in the same CTA combine their split
+// counts, minima and arrivals in shared memory first, so a block of N chunks
+// costs one global arrival / count / cursor atomic per CTA it spans instead
+// of one per chunk (N reaches thousands in the latency-bound rounds, where
+// those same-address atomics serialise in L2).  Two __syncthreads: after
+// tagging (counts published), and after the per-CTA cursor reservation.
+
+struct OnePassSlot {
+    int32_t key;     // big-list index of the warp's block, -1 if none
+    int32_t nsplit;
+    int32_t nkeep;
+    int32_t wmin;
+    int32_t sbase;   // cursor bases reserved by the CTA leader of the block
+    int32_t kbase;
+    int32_t pad[2];
+};
+
+template <int K>
+__device__ __forceinline__ void chunk_place(const SparseParams& p, int32_t bs, int32_t keep, int32_t w,
+                                            const ChunkLane<K>& c, const unsigned* bal, const unsigned* kb,
+                                            int32_t sbase, int32_t kbase) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = lanemask_lt();
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        if (c.valid[j]) {
+            const int32_t np = c.sp[j] ? bs + keep + sbase + __popc(bal[j] & lt) : bs + kbase + __popc(kb[j] & lt);
+            p.members[np] = c.r[j];
+            if (c.sp[j]) p.block[c.r[j].x] = w;
+        }
+        sbase += __popc(bal[j]);
+        kbase += __popc(kb[j]);
+    }
+    (void)lane;
+}
+
+template <bool IDENT, int K>
+__device__ int32_t big_onepass_cta(const SparseParams& p, int cur, int64_t round, int32_t C, int32_t nbig,
+                                   int32_t ci, OnePassSlot* slot) {
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    const bool has = ci >= 0;
+    int32_t k = -1, l = 0, bs = 0, bz = 0, ci0 = 0, ol = 0, nrl = 0;
+    ChunkLane<K> c;
+    unsigned bal[K], kb[K];
+    int32_t nsplit = 0, nkeep = 0, wmin = kBig;
+    if (has) {
+        k = find_owner<K>(p, nbig, ci);
+        const int4 e = big_list_of<K>(p)[k];
+        l = e.x;
+        bs = e.y;
+        bz = e.z;
+        ci0 = (ci - e.w) * (32 * K);
+        leader_slots<IDENT>(p, l, ol, nrl);
+        chunk_tag<IDENT, K>(p, l, bs, bz, ci0, ol, nrl, c);
+        chunk_counts<K>(c, bal, kb, nsplit, nkeep, wmin);
+    } else {
+#pragma unroll
+        for (int j = 0; j < K; ++j) c.valid[j] = false;
+    }
+    if (lane == 0) {
+        OnePassSlot& m = slot[wid];
+        m.key = k;
+        m.nsplit = nsplit;
+        m.nkeep = nkeep;
+        m.wmin = wmin;
+    }
+    __syncthreads();
+    int32_t leader = wid, cnt_cta = 1, tot_s = nsplit, tot_k = nkeep, pre_s = 0, pre_k = 0, mn = wmin;
+    int32_t ns = 0, w = kBig, nch_b = 1;
+    if (has) {
+        const OnePassSlot o = slot[lane];  // kSparseThreads / 32 == 32 slots, one per lane
+        const bool same = o.key == k;
+        const unsigned msk = __ballot_sync(kFull, same);
+        leader = __ffs(msk) - 1;
+        cnt_cta = __popc(msk);
+        tot_s = __reduce_add_sync(kFull, same ? o.nsplit : 0);
+        tot_k = __reduce_add_sync(kFull, same ? o.nkeep : 0);
+        mn = __reduce_min_sync(kFull, same ? o.wmin : kBig);
+        pre_s = __reduce_add_sync(kFull, (same && lane < wid) ? o.nsplit : 0);
+        pre_k = __reduce_add_sync(kFull, (same && lane < wid) ? o.nkeep : 0);
+        nch_b = (bz + 32 * K - 1) / (32 * K);
+        if (nch_b > cnt_cta) {  // the block spans CTAs: combine globally
+            if (lane == 0) {
+                if (wid == leader) {
+                    if (tot_s) {
+                        red_add(&p.scnt[l], tot_s);
+                        red_min(&p.smin[l], mn);
+                    }
+                    // release: count and minimum are visible before the arrival
+                    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(&p.sarr[l]), "r"(cnt_cta)
+                                 : "memory");
+                }
+                while (ld_acquire_u32((const unsigned*)&p.sarr[l]) < (unsigned)nch_b) {
+                }
+                ns = ld_vol(&p.scnt[l]);
+                w = ld_vol(&p.smin[l]);
+            }
+            ns = __shfl_sync(kFull, ns, 0);
+            w = __shfl_sync(kFull, w, 0);
+        } else {
+            ns = tot_s;
+            w = mn;
+        }
+        if (ns && wid == leader && lane == 0) {
+            int32_t sb = 0, kbs = 0;
+            if (nch_b > cnt_cta) {
+                if (tot_s) sb = atomicAdd(&p.scur[l], tot_s);
+                if (tot_k) kbs = atomicAdd(&p.kcur[l], tot_k);
+            }
+            slot[wid].sbase = sb;
+            slot[wid].kbase = kbs;
+        }
+    }
+    __syncthreads();
+    if (has) {
+        if (ns) {
+            const int32_t sb = slot[leader].sbase + pre_s, kbs = slot[leader].kbase + pre_k;
+            chunk_place<K>(p, bs, bz - ns, w, c, bal, kb, sb, kbs);
+            if (ci0 == 0 && lane == 0) finish_block(p, cur, round, C, l, bs, bz, ns, w);
+        }
+        // every chunk of the block has read the leader's marks before anyone
+        // clears: the arrivals above are complete (or the block is in this CTA)
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+            if (c.valid[j]) clear_member<IDENT>(p, c.r[j].x, c.tu[j], slot_base<IDENT>(c.r[j]), nrl);
+        if (ci0 == 0 && lane == 0) red_and(&p.tblock[l >> 5], ~(1u << (l & 31)));
+        return min(32 * K, bz - ci0);
+    }
+    return 0;
+}
+

@@ -20,9 +20,16 @@ constexpr int32_t kSoloMaxC = 64;
 constexpr int32_t kSoloMaxItems = 64;
 constexpr int32_t kSoloSkipSpan = 1024;  // skip-step window of the solo team
 
-template <bool IDENT>
-__global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParams p) {
+template <bool IDENT, bool SH>
+__global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParams pk) {
+    // SH (transition-sharded replica, kernels_shard.cuh): the round-parity
+    // buffers are selected per round on a local copy of the parameters;
+    // otherwise p is the kernel parameter itself
+    SparseParams pl;
+    if (SH) pl = pk;
+    const SparseParams& p = SH ? pl : pk;
     SCtrl* ctl = p.ctrl;
+    unsigned xgen = 0;  // cross-replica barriers passed (SH)
     const int lane = threadIdx.x & 31;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
@@ -33,6 +40,10 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
     const int32_t nwarps = (int32_t)(gsize >> 5);
     unsigned gen = 0;
     __shared__ int32_t s_seen[kSeen];
+    __shared__ long long s_snap[8];  // control words of the current barrier (team_barrier)
+    __shared__ OnePassSlot s_slot[kSparseThreads / 32];
+    int32_t cr_c = -1;               // splitter whose member range cr_v holds
+    int2 cr_v = make_int2(0, 0);
     for (int k = threadIdx.x; k < kSeen; k += blockDim.x) s_seen[k] = -1;
 
     if (gwarp == nwarps - 1) {
@@ -54,7 +65,7 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
     bool try_skip = false;
     int32_t cooldown = 0, backoff = 16;
     int64_t skips = 0;
-    const bool solo_ok = p.allow_solo && p.round_limit == INT64_MAX && gridDim.x > 1;
+    const bool solo_ok = !SH && p.allow_solo && p.round_limit == INT64_MAX && gridDim.x > 1;
     bool solo = false;     // this CTA is in a solo stretch (CTA 0 working, others parked)
     bool fresh = false;    // CTA 0: first solo round of a stretch
     unsigned wakes = 0;    // hand-overs so far; identical on every CTA
@@ -72,6 +83,7 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
             __syncthreads();
             ++wakes;
             solo = false;
+            cr_c = -1;
             if (ld_vol(&ctl->stop)) break;
             C = ld_vol(&ctl->C0);
             round = ld_vol(&ctl->round);
@@ -143,7 +155,7 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
         // the window [C, C + span) is retired at once (0 splits each).  The
         // solo team uses a 1024-label window (one U0 word per warp).
         const int32_t span = solo ? kSoloSkipSpan : kSkipSpan;
-        if (try_skip && p.round_limit == INT64_MAX &&
+        if (!SH && try_skip && p.round_limit == INT64_MAX &&
             (!p.has_guard || (int64_t)p.A + round + span + 1 <= p.max_supersteps)) {
             const int sp = (int)(skips & 1);
             const int32_t lim = (int64_t)C + span < (int64_t)p.n ? C + span : p.n;
@@ -152,9 +164,8 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
                 const bool cand = c >= C && c < lim && ((ld_vol(&p.U0[w]) >> lane) & 1u);
                 if (cand && !round_is_trivial<IDENT>(p, c)) atomicMin(&ctl->nontriv[sp], c);
             }
-            if (solo) __syncthreads();
-            else grid_barrier(p.bar, gen);
-            const int32_t nt = ld_vol(&ctl->nontriv[sp]);
+            team_barrier(solo, p.bar, gen, [&] { s_snap[0] = ld_vol(&ctl->nontriv[sp]); });
+            const int32_t nt = (int32_t)s_snap[0];
             const int32_t end = min(nt, lim);
             int32_t cnt = 0;
             if (end > C) {
@@ -164,7 +175,7 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
                     if (w == (C >> 5)) v &= ~0u << (C & 31);
                     if (w == wlast && (end & 31)) v &= (1u << (end & 31)) - 1u;
                     if (v) {
-                        atomicAnd(&p.U0[w], ~v);
+                        red_and(&p.U0[w], ~v);
                         cnt += __popc(v);
                     }
                 }
@@ -179,11 +190,14 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
                     ctl->skipcnt[sp ^ 1] = 0;
                 }
             }
-            if (solo) __syncthreads();
-            else grid_barrier(p.bar, gen);
-            const int32_t retired = ld_vol(&ctl->skipcnt[sp]);
+            team_barrier(solo, p.bar, gen, [&] {
+                s_snap[1] = ld_vol(&ctl->skipcnt[sp]);
+                s_snap[2] = ld_vol(&ctl->skip_next[sp]);
+            });
+            const int32_t retired = (int32_t)s_snap[1];
             round += retired;
-            C = ld_vol(&ctl->skip_next[sp]);
+            C = (int32_t)s_snap[2];
+            cr_c = -1;
             ++skips;
             if (gtid == 0) ctl->skipped_rounds += (unsigned long long)retired;
             if (retired == 0) {
@@ -197,6 +211,7 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
         }
 
         const int cur = (int)(round & 1), nxt = cur ^ 1;
+        if (SH) shard_select_parity(pl, pk, cur);
         const bool tr = p.trace != nullptr && gtid == 0 && round < p.trace_rounds;
         if (tr) p.trace[round * 8 + 0] = globaltimer();
 
@@ -210,7 +225,7 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
             }
         }
         {
-            const int2 cr = p.brange[C];
+            const int2 cr = cr_c == C ? cr_v : p.brange[C];
             const int32_t cs = cr.x, cz = cr.y;
             // members per warp: spread small splitters one member per warp so
             // their in-edges are walked by as many warps as possible
@@ -249,12 +264,17 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
                         const int32_t e = ej + (k - xj);
                         if (IDENT) {
                             s = p.rev_src[e];
-                            atomicOr(&p.mark[s >> 5], 1u << (s & 31));
+                            if (SH) shard_mark(p, cur, s, -1);
+                            else red_or(&p.mark[s >> 5], 1u << (s & 31));
                         } else {
                             const int2 r = p.rev[e];
                             s = r.y;
-                            atomicOr(&p.mark[r.x >> 5], 1u << (r.x & 31));
-                            atomicOr(&p.touched[s >> 5], 1u << (s & 31));
+                            if (SH) {
+                                shard_mark(p, cur, r.x, s);
+                            } else {
+                                red_or(&p.mark[r.x >> 5], 1u << (r.x & 31));
+                                red_or(&p.touched[s >> 5], 1u << (s & 31));
+                            }
                         }
                     }
                     const int32_t b = act ? p.block[s] : 0;
@@ -262,15 +282,26 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
                     const bool rep = act && lane == __ffs(same) - 1;
                     if (rep && cta_first(s_seen, b)) {
                         const uint32_t bit = 1u << (b & 31);
-                        if (!(ld_vol(&p.tblock[b >> 5]) & bit) && !(atomicOr(&p.tblock[b >> 5], bit) & bit))
+                        if (!(ld_vol(&p.tblock[b >> 5]) & bit) && !(atomicOr(&p.tblock[b >> 5], bit) & bit)) {
                             register_block(p, cur, b);
+                            if (SH) shard_publish(p, cur, b);
+                        }
                     }
                 }
             }
         }
         if (tr) p.trace[round * 8 + 1] = globaltimer();
-        if (solo) __syncthreads();
-        else grid_barrier(p.bar, gen);
+        if (SH) {
+            // every replica's marks are in place; adopt the blocks the other
+            // replicas registered first (kernels_shard.cuh)
+            if (!shard_exchange(p, cur, gen, xgen, s_snap)) break;
+            shard_merge(p, cur, tw, tnw, s_snap);
+        }
+        team_barrier(solo, p.bar, gen, [&] {
+            s_snap[0] = ld_vol(&ctl->n_small[cur]);
+            s_snap[1] = (long long)ld_vol(&ctl->big_pack[cur]);
+            s_snap[2] = (long long)ld_vol(&ctl->big_pack4[cur]);
+        });
         if (tr) {
             p.trace[round * 8 + 2] = globaltimer();
             p.trace[round * 8 + 4] = p.brange[C].y;
@@ -280,9 +311,9 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
         }
 
         // ---- phase B: split the touched blocks ------------------------------
-        const int32_t nsm = ld_vol(&ctl->n_small[cur]);
-        const unsigned long long bp = ld_vol(&ctl->big_pack[cur]);
-        const unsigned long long bp4 = ld_vol(&ctl->big_pack4[cur]);
+        const int32_t nsm = (int32_t)s_snap[0];
+        const unsigned long long bp = (unsigned long long)s_snap[1];
+        const unsigned long long bp4 = (unsigned long long)s_snap[2];
         const int32_t nbig = (int32_t)(bp >> 32), nch1 = (int32_t)(bp & 0xffffffffu);
         const int32_t nch4 = (int32_t)(bp4 & 0xffffffffu);
         if (ttid == 0) {
@@ -291,36 +322,54 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
             ctl->big_pack4[nxt] = 0ull;
             ctl->heavy[nxt] = 0;
             ctl->items_last = nsm + nch1;
+            if (SH) p.peer_xcnt[p.shard][nxt] = 0;
         }
         // chunk layout and pass count for this round (kernels_big.cuh)
         const int mode_b = nsm + nch1 <= tnw ? 0 : (nsm + nch4 <= tnw ? 1 : 2);
         const int32_t nch = mode_b == 0 ? nch1 : nch4;
-        for (int32_t it = tw; it < nsm + nch; it += tnw) {
-            int32_t cnt;
-            if (it < nsm) cnt = process_small<IDENT>(p, cur, round, C, p.small_list[it]);
-            else if (mode_b == 0) cnt = big_onepass<IDENT, 1>(p, cur, round, C, nbig, it - nsm);
-            else if (mode_b == 1) cnt = big_onepass<IDENT, kWide>(p, cur, round, C, nbig, it - nsm);
-            else cnt = big_tag<IDENT, kWide>(p, nbig, it - nsm);
+        if (mode_b == 2) {
+            for (int32_t it = tw; it < nsm + nch; it += tnw) {
+                int32_t cnt;
+                if (it < nsm) cnt = process_small<IDENT>(p, cur, round, C, p.small_list[it]);
+                else cnt = big_tag<IDENT, kWide>(p, nbig, it - nsm);
+                if (lane == 0) my_members += (unsigned long long)cnt;
+            }
+            team_barrier(solo, p.bar, gen, [] {});
+            for (int32_t it = tw; it < nch; it += tnw) big_split<IDENT, kWide>(p, cur, round, C, nbig, it);
+        } else {
+            // one pass: every work item has its own warp; all warps of the
+            // CTA take part (the big-chunk path synchronises the CTA)
+            int32_t cnt = 0;
+            if (tw < nsm) cnt = process_small<IDENT>(p, cur, round, C, p.small_list[tw]);
+            const int32_t ci = tw >= nsm && tw < nsm + nch ? tw - nsm : -1;
+            if (mode_b == 0) cnt += big_onepass_cta<IDENT, 1>(p, cur, round, C, nbig, ci, s_slot);
+            else cnt += big_onepass_cta<IDENT, kWide>(p, cur, round, C, nbig, ci, s_slot);
             if (lane == 0) my_members += (unsigned long long)cnt;
         }
-        if (mode_b == 2) {
-            if (solo) __syncthreads();
-            else grid_barrier(p.bar, gen);
-            for (int32_t it = tw; it < nch; it += tnw) big_split<IDENT, kWide>(p, cur, round, C, nbig, it);
-        }
         for (int k = threadIdx.x; k < kSeen; k += blockDim.x) s_seen[k] = -1;
-        if (solo) __syncthreads();
-        else grid_barrier(p.bar, gen);
+        team_barrier(solo, p.bar, gen, [&] {
+            const int32_t c_next = min(ld_vol(&ctl->next_min[cur]), ld_vol(&ctl->succ[cur]));
+            s_snap[3] = c_next;
+            s_snap[4] = ld_vol(&ctl->heavy[cur]);
+            s_snap[5] = ld_vol(&ctl->items_last);
+            if (c_next != kBig) {
+                const int32_t* r = (const int32_t*)&p.brange[c_next];
+                s_snap[6] = ((long long)ld_vol(r + 1) << 32) | (unsigned)ld_vol(r);
+            }
+        });
         if (tr) p.trace[round * 8 + 3] = globaltimer();
-        C = min(ld_vol(&ctl->next_min[cur]), ld_vol(&ctl->succ[cur]));
+        C = (int32_t)s_snap[3];
+        if (C != kBig) {
+            cr_c = C;
+            cr_v = make_int2((int32_t)(s_snap[6] & 0xffffffffll), (int32_t)(s_snap[6] >> 32));
+        }
         ++round;
         if (cooldown > 0) --cooldown;
-        try_skip = p.allow_skip && cooldown == 0 && ld_vol(&ctl->heavy[cur]) == 0;
-
+        try_skip = p.allow_skip && cooldown == 0 && s_snap[4] == 0;
 
         // ---- grid team: go solo for the next rounds? (uniform decision) ----
-        if (!solo && solo_ok && !try_skip && C != kBig && p.brange[C].y <= kSoloMaxC &&
-            ld_vol(&ctl->items_last) <= kSoloMaxItems) {
+        if (!solo && solo_ok && !try_skip && C != kBig && cr_v.y <= kSoloMaxC &&
+            (int32_t)s_snap[5] <= kSoloMaxItems) {
             solo = true;  // CTA 0 continues alone, the others park at the loop head
             fresh = true;
             ++stretches;

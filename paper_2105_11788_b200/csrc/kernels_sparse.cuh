@@ -29,6 +29,7 @@
 namespace bisim {
 
 constexpr int kSparseThreads = 1024;  // one CTA per SM
+constexpr int kMaxShards = 8;         // replicas of the transition-sharded mode
 
 // Grid barrier: one monotonic arrival counter; CTA leaders add with
 // acq_rel semantics and spin (ld.acquire) until it reaches this barrier's
@@ -55,6 +56,26 @@ __device__ __forceinline__ void grid_barrier(GridBarrier* gb, unsigned& gen) {
         }
     }
     ++gen;
+    __syncthreads();
+}
+
+// Team barrier plus a control snapshot: after the barrier, thread 0 of each
+// CTA runs snap() (reading the round's control words once per CTA into
+// shared memory) before the CTA is released, so the 1024 threads of a CTA
+// never all load the same global words.  solo: the team is this CTA alone.
+template <typename F>
+__device__ __forceinline__ void team_barrier(bool solo, GridBarrier* gb, unsigned& gen, F&& snap) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (!solo) {
+            const unsigned target = (gen + 1) * gridDim.x;
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&gb->count) : "memory");
+            while ((int)(ld_acquire_u32(&gb->count) - target) < 0) {
+            }
+        }
+        snap();
+    }
+    if (!solo) ++gen;
     __syncthreads();
 }
 
@@ -141,6 +162,19 @@ struct SparseParams {
     int32_t cta_minor;          // spread consecutive work items over SMs
     int32_t allow_solo;         // small rounds on CTA 0 alone (kernels_loop.cuh)
     int32_t pad3;
+    // ---- transition-sharded mode (kernels_shard.cuh); nshard == 1 otherwise
+    int32_t nshard;                       // replicas taking part in every round
+    int32_t shard;                        // my index
+    int64_t mark_stride;                  // words from the parity-0 to the parity-1 mark buffer
+    int64_t bm_stride;                    // same for the touched / tblock bitmaps
+    uint32_t* peer_mark[kMaxShards];      // every replica's mark / touched buffers (parity 0)
+    uint32_t* peer_touched[kMaxShards];
+    int32_t* xlist;                       // [2][n] blocks this replica registered first, by parity
+    int32_t* peer_xlist[kMaxShards];
+    int32_t* peer_xcnt[kMaxShards];       // [2] lengths of those lists
+    unsigned* peer_xbar[kMaxShards];      // cross-replica arrival counters
+    unsigned* go;                         // release word of the combined barrier (local)
+    unsigned long long timeout_ns;        // give up a cross-replica wait after this long
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -155,9 +189,9 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // bit may be set redundantly; it only has to be set whenever its range is
 // non-empty).
 __device__ __forceinline__ void u_set(const SparseParams& p, int32_t x) {
-    atomicOr(&p.U0[x >> 5], 1u << (x & 31));
-    atomicOr(&p.U1[x >> 15], 1u << ((x >> 10) & 31));
-    atomicOr(&p.U2[x >> 25], 1u << ((x >> 20) & 31));
+    red_or(&p.U0[x >> 5], 1u << (x & 31));
+    red_or(&p.U1[x >> 15], 1u << ((x >> 10) & 31));
+    red_or(&p.U2[x >> 25], 1u << ((x >> 20) & 31));
 }
 
 // Clear x (whole warp participates; no concurrent raises in this phase).
@@ -179,7 +213,7 @@ __device__ __forceinline__ void u_clear_warp(const SparseParams& p, int32_t x) {
     const int32_t wj = (d << 5) + lane;
     v = wj < p.nw1 ? p.U1[wj] : 0u;
     if (__ballot_sync(kFull, v != 0u)) return;
-    if (lane == 0) atomicAnd(&p.U2[d >> 5], ~(1u << (d & 31)));
+    if (lane == 0) red_and(&p.U2[d >> 5], ~(1u << (d & 31)));
 }
 
 // Smallest unstable label >= from (kBig if none); whole warp participates.
@@ -324,15 +358,15 @@ __device__ __forceinline__ void clear_member(const SparseParams& p, int32_t u, b
                                              int32_t nr) {
     if (!tu) return;
     if (IDENT) {
-        atomicAnd(&p.mark[u >> 5], ~(1u << (u & 31)));
+        red_and(&p.mark[u >> 5], ~(1u << (u & 31)));
         return;
     }
-    atomicAnd(&p.touched[u >> 5], ~(1u << (u & 31)));
+    red_and(&p.touched[u >> 5], ~(1u << (u & 31)));
     int32_t pos = ou, left = nr;
     while (left > 0) {
         const int32_t sh = pos & 31, len = min(left, 32 - sh);
         const uint32_t msk = (len == 32 ? ~0u : ((1u << len) - 1u)) << sh;
-        atomicAnd(&p.mark[pos >> 5], ~msk);
+        red_and(&p.mark[pos >> 5], ~msk);
         pos += len;
         left -= len;
     }
@@ -347,8 +381,8 @@ __device__ __forceinline__ void raise_split(const SparseParams& p, int cur, int6
         u_set(p, C);
         lo = min(lo, C);
     }
-    atomicMin(&p.ctrl->next_min[cur], lo);
-    if (round < p.splits_cap) atomicAdd(&p.splits[round], 1);
+    red_min(&p.ctrl->next_min[cur], lo);
+    if (round < p.splits_cap) red_add(&p.splits[round], 1);
 }
 
 // A touched block of <= 32 members, finished by one warp.
@@ -384,7 +418,7 @@ __device__ int32_t process_small(const SparseParams& p, int cur, int64_t round, 
     }
     __syncwarp();
     if (valid) clear_member<IDENT>(p, u, tu, ou, nr);
-    if (lane == 0) atomicAnd(&p.tblock[l >> 5], ~(1u << (l & 31)));
+    if (lane == 0) red_and(&p.tblock[l >> 5], ~(1u << (l & 31)));
     return bz;
 }
 
@@ -425,6 +459,7 @@ __device__ __forceinline__ bool round_is_trivial(const SparseParams& p, int32_t 
 
 // ---- the persistent kernel ---------------------------------------------------
 
+#include "kernels_shard.cuh"
 #include "kernels_loop.cuh"
 
 // ---- setup kernels -----------------------------------------------------------
@@ -488,22 +523,27 @@ template <bool BCRP>
 __global__ void k_rev_fill2(int32_t n, int64_t m, const int32_t* __restrict__ src,
                             const int32_t* __restrict__ act, const int32_t* __restrict__ dst,
                             const unsigned long long* __restrict__ lmask, const int32_t* __restrict__ off,
-                            int32_t* cursor, int2* rev, int32_t* rev_src) {
+                            int32_t* cursor, int2* rev, int32_t* rev_src, int32_t lo, int32_t hi) {
+    // only transitions with source in [lo, hi) (the whole range unless sharded)
     const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < m; i0 += stride) {
         const int64_t i = i0 + lane;
         int32_t t = -1 - lane, slot = 0, s = 0;
+        bool in = false;
         if (i < m) {
-            t = dst[i];
             s = src[i];
+            in = s >= lo && s < hi;
+        }
+        if (in) {
+            t = dst[i];
             slot = BCRP ? off[s] + label_rank(lmask, n, s, act[i]) : s;
         }
         const LaneRun run = lane_run(t);
         int32_t base = 0;
-        if (i < m && run.rank == 0) base = atomicAdd(&cursor[t], run.len);
+        if (in && run.rank == 0) base = atomicAdd(&cursor[t], run.len);
         base = __shfl_sync(kFull, base, run.leader);
-        if (i < m) {
+        if (in) {
             const int32_t at = base + run.rank;
             if (BCRP) rev[at] = make_int2(slot, s);
             else rev_src[at] = s;
