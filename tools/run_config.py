@@ -15,7 +15,11 @@ from paper_2105_11788_b200 import bcrp_arrays, rcpp_arrays  # noqa: E402
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c1"
 mode = {"sparse": N.MODE_AUTO, "dense": N.MODE_DENSE}[sys.argv[2] if len(sys.argv) > 2 else "sparse"]
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 1
-inst, desc = make_instance(cfg, 0)
+if cfg.startswith("chain"):  # e.g. chain50000: a smaller c3 for profiling
+    from paper_2105_11788_b200 import workloads as W
+    inst, desc = W.chain(int(cfg[5:])), cfg
+else:
+    inst, desc = make_instance(cfg, 0)
 for _ in range(reps):
     t = time.perf_counter()
     if inst.kind == "bcrp":
