@@ -56,6 +56,9 @@ def make_instance(config: str, rank: int):
         return W.c4_uniform(seed=4 + rank), "c4_uniform: n=5M m=50M |Act|=256 iid"
     if config == "c4l":
         return W.c4_lifted(seed=44 + rank), "c4_lifted: n=5M m=50M |Act|=256 lifted quotient"
+    if config == "c5s":
+        return (W.c5_vlts(n=40_000_000, k=20_000, seed=40),
+                "c5_sharded: lifted quotient n=40M m=400M |Act|=32 k=20000, one LTS")
     raise SystemExit(f"unknown config {config}")
 
 
@@ -388,18 +391,91 @@ def run_b200(args):
     return 0
 
 
+def run_sharded_bench(args):
+    """One LTS split over the replicas of the transition-sharded mode
+    (csrc/kernels_shard.cuh): devices 0..gpus-1, or `--virtual K` replicas
+    sharing device 0 (correctness/overhead only).  Under torchrun rank 0
+    drives every device and the other ranks only wait."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2105_11788_b200.sharded import bcrp_sharded_arrays, rcpp_sharded_arrays
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    if rank != 0:
+        dist.barrier()
+        dist.destroy_process_group()
+        return 0
+    devices = [0] * args.virtual if args.virtual else list(range(args.gpus))
+    inst, desc = make_instance(args.config, 0)
+
+    def step():
+        if inst.kind == "bcrp":
+            return bcrp_sharded_arrays(inst.n, inst.src, inst.act, inst.dst, inst.num_actions,
+                                       devices)
+        return rcpp_sharded_arrays(inst.n, inst.src, inst.dst, inst.pi0, devices)
+
+    for _ in range(args.warmup):
+        block, st, ns = step()
+    correct = None if inst.truth is None else bool(np.array_equal(block, inst.truth))
+    if correct is False:
+        raise SystemExit("bench: sharded result differs from the known coarsest partition")
+    dev_ms, wall_ms = [], []
+    with ClockSampler(0) as clocks:
+        for _ in range(args.steps):
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            block, st, ns = step()
+            wall_ms.append((time.perf_counter() - t) * 1e3)
+            dev_ms.append(ns["t_pre_ms"] + ns["t_label_ms"] + ns["t_alg_ms"])
+    ms = statistics.mean(dev_ms)
+    units = inst.n + inst.m
+    line = {
+        "metric": METRIC, "value": units / (ms / 1e3), "unit": UNIT, "n_gpus": len(set(devices)),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": desc, "n": inst.n, "m": inst.m, "supersteps": st.supersteps,
+                   "parallelism": f"transition-sharded x{len(devices)} replicas on devices {devices}",
+                   "correct_vs_truth": correct},
+        "per_round_us": ns["t_alg_ms"] * 1e3 / max(st.supersteps, 1),
+        "phase_ms": {"pre": ns["t_pre_ms"], "label": ns["t_label_ms"], "alg": ns["t_alg_ms"]},
+        "e2e": {"value": units / (statistics.mean(wall_ms) / 1e3), "unit": UNIT,
+                "ms_per_step": statistics.mean(wall_ms),
+                "h2d_bytes_per_step": int(12 * inst.m * len(devices)),
+                "d2h_bytes_per_step": int(4 * inst.n + 4 * st.supersteps)},
+        "clocks": clocks.summary(),
+        "gpu_launches": int(ns["kernel_launches"]) * args.steps,  # loop kernels (one per replica)
+        "note": "value: device time of preprocessing + label rounds + loop (max over replicas); "
+                "inputs copied to every replica inside e2e",
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c5", choices=["c5", "c1", "c2", "c3", "c4u", "c4l"])
+    ap.add_argument("--config", default="c5", choices=["c5", "c1", "c2", "c3", "c4u", "c4l", "c5s"])
+    ap.add_argument("--sharded", action="store_true",
+                    help="one LTS over --gpus devices (transition-sharded mode)")
+    ap.add_argument("--virtual", type=int, default=0,
+                    help="with --sharded: this many replicas sharing GPU 0 (testing)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.sharded:
+        return run_sharded_bench(args)
     return run_b200(args)
 
 

@@ -70,7 +70,7 @@ struct Ctx {
     DevBuf src, act, dst, pi0, lmask, off, rev_ptr, cursor, rev_slot, block, nl, mark, unstable,
         split_list, cmem, splits, ctrl, scan_tmp, rev2, members, bstart, bsize, touched, tblock,
         small_list, big_list, big_base, tmp, scnt, smin, kcur, scur, counter, brange, bar, trace, lhash, lkeys,
-        lmins, sarr, big_list4, big_base4;
+        lmins, sarr, big_list4, big_base4, big_info, big_info4;
     int launches = 0;
 };
 
@@ -480,6 +480,8 @@ int run_with(Ctx& c, Job& j) {
         sp.big_base = (int32_t*)c.big_base.ensure(((int64_t)n / 32 + 2) * 4);
         sp.big_list4 = (int4*)c.big_list4.ensure(((int64_t)n / 32 + 2) * 16);
         sp.big_base4 = (int32_t*)c.big_base4.ensure(((int64_t)n / 32 + 2) * 4);
+        sp.big_info = (int2*)c.big_info.ensure(((int64_t)n / 32 + 2) * 8);
+        sp.big_info4 = (int2*)c.big_info4.ensure(((int64_t)n / 32 + 2) * 8);
         sp.tmp = (MemberRec*)c.tmp.ensure((int64_t)n * sizeof(MemberRec));
         sp.scnt = (int32_t*)c.scnt.ensure((int64_t)n * 4);
         sp.smin = (int32_t*)c.smin.ensure((int64_t)n * 4);
@@ -497,8 +499,8 @@ int run_with(Ctx& c, Job& j) {
         // developer tracing: BISIM_TRACE=<rounds> BISIM_TRACE_FILE=<path>
         if (const char* tr = getenv("BISIM_TRACE")) {
             sp.trace_rounds = atoll(tr);
-            sp.trace = (unsigned long long*)c.trace.ensure(sp.trace_rounds * 64 + 64);
-            CK(cudaMemsetAsync(sp.trace, 0, sp.trace_rounds * 64, st));
+            sp.trace = (unsigned long long*)c.trace.ensure(sp.trace_rounds * 8 * kTraceWords + 64);
+            CK(cudaMemsetAsync(sp.trace, 0, sp.trace_rounds * 8 * kTraceWords, st));
         }
     }
     CK(cudaGetLastError());
@@ -623,15 +625,18 @@ int run_with(Ctx& c, Job& j) {
     S.t_d2h_ms = elapsed(c.ev[4], c.ev[5]);
     S.bytes_alg = loop_bytes(j.bcrp, dense, n, L32, R, ls);
     if (!dense && sp.trace) {
-        std::vector<unsigned long long> t(sp.trace_rounds * 8);
+        std::vector<unsigned long long> t(sp.trace_rounds * kTraceWords);
         CK(cudaMemcpy(t.data(), sp.trace, t.size() * 8, cudaMemcpyDeviceToHost));
         const char* path = getenv("BISIM_TRACE_FILE");
         if (FILE* f = fopen(path ? path : "bisim_trace.csv", "w")) {
-            fprintf(f, "round,phaseA_ns,barrierA_ns,phaseB_ns,csize,w0_edges_cum,n_small,big_chunks,n_big\n");
+            fprintf(f, "round,phaseA_ns,barrierA_ns,phaseB_ns,csize,solo,n_small,big_chunks,n_big,"
+                       "b_tag_ns,b_sync1_ns,b_arrive_ns,b_sync2_ns,b_place_ns\n");
             for (int64_t r = 0; r < std::min<int64_t>(sp.trace_rounds, R); ++r) {
-                const unsigned long long* q = &t[r * 8];
-                fprintf(f, "%lld,%llu,%llu,%llu,%llu,%llu,%llu,%llu,%llu\n", (long long)r, q[1] - q[0], q[2] - q[1],
-                        q[3] - q[2], q[4], q[5], q[6], q[7] & 0xffffffffull, q[7] >> 32);
+                const unsigned long long* q = &t[r * kTraceWords];
+                auto d = [&](int a, int b) -> long long { return (q[a] && q[b]) ? (long long)(q[a] - q[b]) : -1; };
+                fprintf(f, "%lld,%llu,%llu,%llu,%llu,%llu,%llu,%llu,%llu,%lld,%lld,%lld,%lld,%lld\n", (long long)r,
+                        q[1] - q[0], q[2] - q[1], q[3] - q[2], q[4], q[5], q[6], q[7] & 0xffffffffull, q[7] >> 32,
+                        d(8, 2), d(9, 8), d(10, 9), d(11, 10), d(12, 11));
             }
             fclose(f);
         }

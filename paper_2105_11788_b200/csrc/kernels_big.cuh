@@ -27,6 +27,10 @@ template <int K>
 __device__ __forceinline__ const int32_t* big_base_of(const SparseParams& p) {
     return K == 1 ? p.big_base : p.big_base4;
 }
+template <int K>
+__device__ __forceinline__ const int2* big_info_of(const SparseParams& p) {
+    return K == 1 ? p.big_info : p.big_info4;
+}
 
 // Owner (list index) of chunk ci: the last big block whose first chunk <= ci.
 template <int K>
@@ -190,10 +194,11 @@ __device__ __forceinline__ void leader_slots(const SparseParams& p, int32_t l, i
 template <bool IDENT, int K>
 __device__ int32_t big_tag(const SparseParams& p, int32_t nbig, int32_t ci) {
     const int lane = threadIdx.x & 31;
-    const int4 e = big_list_of<K>(p)[find_owner<K>(p, nbig, ci)];
+    const int32_t k = find_owner<K>(p, nbig, ci);
+    const int4 e = big_list_of<K>(p)[k];
+    const int2 li = big_info_of<K>(p)[k];
     const int32_t l = e.x, bs = e.y, bz = e.z, ci0 = (ci - e.w) * (32 * K);
-    int32_t ol, nrl;
-    leader_slots<IDENT>(p, l, ol, nrl);
+    const int32_t ol = li.x, nrl = li.y;
     ChunkLane<K> c;
     chunk_tag<IDENT, K>(p, l, bs, bz, ci0, ol, nrl, c);
 #pragma unroll
@@ -218,10 +223,10 @@ template <bool IDENT, int K>
 __device__ void big_split(const SparseParams& p, int cur, int64_t round, int32_t C, int32_t nbig,
                           int32_t ci) {
     const int lane = threadIdx.x & 31;
-    const int4 e = big_list_of<K>(p)[find_owner<K>(p, nbig, ci)];
+    const int32_t k = find_owner<K>(p, nbig, ci);
+    const int4 e = big_list_of<K>(p)[k];
     const int32_t l = e.x, bs = e.y, bz = e.z, ci0 = (ci - e.w) * (32 * K);
-    int32_t ol, nrl;
-    leader_slots<IDENT>(p, l, ol, nrl);
+    const int32_t nrl = big_info_of<K>(p)[k].y;
     ChunkLane<K> c;
     uint32_t tw[K];
 #pragma unroll
@@ -259,10 +264,11 @@ template <bool IDENT, int K>
 __device__ int32_t big_onepass(const SparseParams& p, int cur, int64_t round, int32_t C, int32_t nbig,
                                int32_t ci) {
     const int lane = threadIdx.x & 31;
-    const int4 e = big_list_of<K>(p)[find_owner<K>(p, nbig, ci)];
+    const int32_t k = find_owner<K>(p, nbig, ci);
+    const int4 e = big_list_of<K>(p)[k];
+    const int2 li = big_info_of<K>(p)[k];
     const int32_t l = e.x, bs = e.y, bz = e.z, ci0 = (ci - e.w) * (32 * K);
-    int32_t ol, nrl;
-    leader_slots<IDENT>(p, l, ol, nrl);
+    const int32_t ol = li.x, nrl = li.y;
     ChunkLane<K> c;
     chunk_tag<IDENT, K>(p, l, bs, bz, ci0, ol, nrl, c);
     unsigned bal[K], kb[K];
@@ -351,17 +357,20 @@ __device__ int32_t big_onepass_cta(const SparseParams& p, int cur, int64_t round
     if (has) {
         k = find_owner<K>(p, nbig, ci);
         const int4 e = big_list_of<K>(p)[k];
+        const int2 li = big_info_of<K>(p)[k];
         l = e.x;
         bs = e.y;
         bz = e.z;
         ci0 = (ci - e.w) * (32 * K);
-        leader_slots<IDENT>(p, l, ol, nrl);
+        ol = li.x;
+        nrl = li.y;
         chunk_tag<IDENT, K>(p, l, bs, bz, ci0, ol, nrl, c);
         chunk_counts<K>(c, bal, kb, nsplit, nkeep, wmin);
     } else {
 #pragma unroll
         for (int j = 0; j < K; ++j) c.valid[j] = false;
     }
+    trace_at(p, round, 8);
     if (lane == 0) {
         OnePassSlot& m = slot[wid];
         m.key = k;
@@ -370,6 +379,7 @@ __device__ int32_t big_onepass_cta(const SparseParams& p, int cur, int64_t round
         m.wmin = wmin;
     }
     __syncthreads();
+    trace_at(p, round, 9);
     int32_t leader = wid, cnt_cta = 1, tot_s = nsplit, tot_k = nkeep, pre_s = 0, pre_k = 0, mn = wmin;
     int32_t ns = 0, w = kBig, nch_b = 1;
     if (has) {
@@ -406,6 +416,7 @@ __device__ int32_t big_onepass_cta(const SparseParams& p, int cur, int64_t round
             ns = tot_s;
             w = mn;
         }
+        trace_at(p, round, 10);
         if (ns && wid == leader && lane == 0) {
             int32_t sb = 0, kbs = 0;
             if (nch_b > cnt_cta) {
@@ -417,6 +428,7 @@ __device__ int32_t big_onepass_cta(const SparseParams& p, int cur, int64_t round
         }
     }
     __syncthreads();
+    trace_at(p, round, 11);
     if (has) {
         if (ns) {
             const int32_t sb = slot[leader].sbase + pre_s, kbs = slot[leader].kbase + pre_k;
@@ -429,6 +441,7 @@ __device__ int32_t big_onepass_cta(const SparseParams& p, int cur, int64_t round
         for (int j = 0; j < K; ++j)
             if (c.valid[j]) clear_member<IDENT>(p, c.r[j].x, c.tu[j], slot_base<IDENT>(c.r[j]), nrl);
         if (ci0 == 0 && lane == 0) red_and(&p.tblock[l >> 5], ~(1u << (l & 31)));
+        trace_at(p, round, 12);
         return min(32 * K, bz - ci0);
     }
     return 0;

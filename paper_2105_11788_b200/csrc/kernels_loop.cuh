@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
         const int cur = (int)(round & 1), nxt = cur ^ 1;
         if (SH) shard_select_parity(pl, pk, cur);
         const bool tr = p.trace != nullptr && gtid == 0 && round < p.trace_rounds;
-        if (tr) p.trace[round * 8 + 0] = globaltimer();
+        if (tr) p.trace[round * kTraceWords + 0] = globaltimer();
 
         // ---- phase A: mark the in-edges of C's members ----------------------
         if (aux) {
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
                 }
             }
         }
-        if (tr) p.trace[round * 8 + 1] = globaltimer();
+        if (tr) p.trace[round * kTraceWords + 1] = globaltimer();
         if (SH) {
             // every replica's marks are in place; adopt the blocks the other
             // replicas registered first (kernels_shard.cuh)
@@ -303,11 +303,11 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
             s_snap[2] = (long long)ld_vol(&ctl->big_pack4[cur]);
         });
         if (tr) {
-            p.trace[round * 8 + 2] = globaltimer();
-            p.trace[round * 8 + 4] = p.brange[C].y;
-            p.trace[round * 8 + 5] = solo ? 1 : 0;
-            p.trace[round * 8 + 6] = ld_vol(&ctl->n_small[cur]);
-            p.trace[round * 8 + 7] = ld_vol(&ctl->big_pack[cur]);
+            p.trace[round * kTraceWords + 2] = globaltimer();
+            p.trace[round * kTraceWords + 4] = p.brange[C].y;
+            p.trace[round * kTraceWords + 5] = solo ? 1 : 0;
+            p.trace[round * kTraceWords + 6] = ld_vol(&ctl->n_small[cur]);
+            p.trace[round * kTraceWords + 7] = ld_vol(&ctl->big_pack[cur]);
         }
 
         // ---- phase B: split the touched blocks ------------------------------
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
                 s_snap[6] = ((long long)ld_vol(r + 1) << 32) | (unsigned)ld_vol(r);
             }
         });
-        if (tr) p.trace[round * 8 + 3] = globaltimer();
+        if (tr) p.trace[round * kTraceWords + 3] = globaltimer();
         C = (int32_t)s_snap[3];
         if (C != kBig) {
             cr_c = C;

@@ -147,6 +147,8 @@ struct SparseParams {
     int32_t* big_base;    // first chunk of each big touched block (ascending)
     int4* big_list4;      // the same blocks in the kWide chunk layout
     int32_t* big_base4;
+    int2* big_info;       // leader slot base / slot count of each big_list entry
+    int2* big_info4;      // same for big_list4
     int4* tmp;            // per member position: the record, x = -1-state if split
     int32_t* scnt;        // per label: split count / min split / compaction cursors
     int32_t* smin;
@@ -181,6 +183,16 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
+}
+
+// Developer trace (BISIM_TRACE): kTraceWords words per round, written by
+// thread 0 of CTA 0: [0..3] round start / end of phase A / after the A
+// barrier / after the B barrier, [4..7] counters, [8..12] phase-B steps of
+// the one-pass path (tagged, CTA-synced, arrived, cursors synced, done).
+constexpr int kTraceWords = 16;
+__device__ __forceinline__ void trace_at(const SparseParams& p, int64_t round, int k) {
+    if (p.trace && blockIdx.x == 0 && threadIdx.x == 0 && round < p.trace_rounds)
+        p.trace[round * kTraceWords + k] = globaltimer();
 }
 
 // ---- hierarchical unstable set --------------------------------------------
@@ -271,6 +283,10 @@ __device__ int32_t u_next_warp(const SparseParams& p, int32_t from) {
 __device__ __forceinline__ void register_block(const SparseParams& p, int cur, int32_t b) {
     SCtrl* ctl = p.ctrl;
     const int2 r = p.brange[b];
+    // leader slot range, loaded alongside the range (phase B then reads it
+    // with the list entry instead of after it)
+    const int32_t ob = p.off ? p.off[b] : b;
+    const int32_t nb = p.off ? p.off[b + 1] - ob : 1;
     if (r.y > 1) ctl->heavy[cur] = 1;
     if (r.y <= 32) {
         const int32_t k = atomicAdd(&ctl->n_small[cur], 1);
@@ -287,8 +303,10 @@ __device__ __forceinline__ void register_block(const SparseParams& p, int cur, i
         const int32_t k4 = (int32_t)(pk4 >> 32), base4 = (int32_t)(pk4 & 0xffffffffu);
         p.big_list[k] = make_int4(b, r.x, r.y, base);
         p.big_base[k] = base;
+        p.big_info[k] = make_int2(ob, nb);
         p.big_list4[k4] = make_int4(b, r.x, r.y, base4);
         p.big_base4[k4] = base4;
+        p.big_info4[k4] = make_int2(ob, nb);
         p.scnt[b] = 0;
         p.smin[b] = kBig;
         p.kcur[b] = 0;
