@@ -496,6 +496,8 @@ int run_with(Ctx& c, Job& j) {
         sp.cta_minor = getenv("BISIM_CTA_MAJOR") == nullptr ? 1 : 0;
         // BISIM_NO_SOLO=1 keeps every round on the whole grid
         sp.allow_solo = getenv("BISIM_NO_SOLO") == nullptr ? 1 : 0;
+        // developer: BISIM_MODE_B=1|2 forces the wide / two-pass phase-B layout
+        sp.force_mode_b = getenv("BISIM_MODE_B") ? atoi(getenv("BISIM_MODE_B")) : -1;
         // developer tracing: BISIM_TRACE=<rounds> BISIM_TRACE_FILE=<path>
         if (const char* tr = getenv("BISIM_TRACE")) {
             sp.trace_rounds = atoll(tr);

@@ -325,7 +325,12 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
             if (SH) p.peer_xcnt[p.shard][nxt] = 0;
         }
         // chunk layout and pass count for this round (kernels_big.cuh)
-        const int mode_b = nsm + nch1 <= tnw ? 0 : (nsm + nch4 <= tnw ? 1 : 2);
+        int mode_b = nsm + nch1 <= tnw ? 0 : (nsm + nch4 <= tnw ? 1 : 2);
+        // a few very large blocks (> 16K members each on average): the wide
+        // layout keeps a quarter of the warps busy with 4 loads in flight per
+        // lane, which measured faster than every warp holding one chunk
+        if (mode_b == 0 && nch1 > 512 * nbig) mode_b = 1;
+        if (p.force_mode_b > mode_b) mode_b = p.force_mode_b;
         const int32_t nch = mode_b == 0 ? nch1 : nch4;
         if (mode_b == 2) {
             for (int32_t it = tw; it < nsm + nch; it += tnw) {

@@ -163,7 +163,7 @@ struct SparseParams {
     int32_t allow_skip;         // retire runs of no-op rounds in one step
     int32_t cta_minor;          // spread consecutive work items over SMs
     int32_t allow_solo;         // small rounds on CTA 0 alone (kernels_loop.cuh)
-    int32_t pad3;
+    int32_t force_mode_b;       // developer override of the phase-B layout (-1: automatic)
     // ---- transition-sharded mode (kernels_shard.cuh); nshard == 1 otherwise
     int32_t nshard;                       // replicas taking part in every round
     int32_t shard;                        // my index
