@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
     int32_t cr_c = -1;               // splitter whose member range cr_v holds
     int2 cr_v = make_int2(0, 0);
     for (int k = threadIdx.x; k < kSeen; k += blockDim.x) s_seen[k] = -1;
+    raise_init();
 
     if (gwarp == nwarps - 1) {
         const int32_t c = u_next_warp(p, 0);
@@ -217,11 +218,13 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
 
         // ---- phase A: mark the in-edges of C's members ----------------------
         if (aux) {
-            u_clear_warp(p, C);
-            const int32_t sc = u_next_warp(p, C + 1);
+            const int32_t sc = u_clear_next_warp(p, C);
             if (lane == 0) {
                 ctl->succ[cur] = sc;
                 ctl->next_min[cur] = kBig;
+                // the usual next splitter: fetch its member range now (it
+                // cannot change this round unless the label is raised again)
+                if (sc != kBig) ctl->succ_range[cur] = p.brange[sc];
             }
         }
         {
@@ -280,13 +283,18 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
                     const int32_t b = act ? p.block[s] : 0;
                     const unsigned same = __match_any_sync(kFull, act ? b : -1 - lane);
                     const bool rep = act && lane == __ffs(same) - 1;
-                    if (rep && cta_first(s_seen, b)) {
-                        const uint32_t bit = 1u << (b & 31);
-                        if (!(ld_vol(&p.tblock[b >> 5]) & bit) && !(atomicOr(&p.tblock[b >> 5], bit) & bit)) {
-                            register_block(p, cur, b);
-                            if (SH) shard_publish(p, cur, b);
+                    bool reg = false;
+                    if (rep) {
+                        const int f = cta_first(s_seen, b);
+                        if (f == 1 && solo) {
+                            reg = true;  // the solo team is this CTA: its table is exact
+                        } else if (f) {
+                            const uint32_t bit = 1u << (b & 31);
+                            reg = !(ld_vol(&p.tblock[b >> 5]) & bit) && !(atomicOr(&p.tblock[b >> 5], bit) & bit);
                         }
                     }
+                    register_blocks_warp(p, cur, reg, b);
+                    if (SH && reg) shard_publish(p, cur, b);
                 }
             }
         }
@@ -352,14 +360,21 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
             if (lane == 0) my_members += (unsigned long long)cnt;
         }
         for (int k = threadIdx.x; k < kSeen; k += blockDim.x) s_seen[k] = -1;
-        team_barrier(solo, p.bar, gen, [&] {
-            const int32_t c_next = min(ld_vol(&ctl->next_min[cur]), ld_vol(&ctl->succ[cur]));
+        team_barrier(solo, p.bar, gen, [&] { raise_flush_warp0(p, cur, round); }, [&] {
+            const int32_t nm = ld_vol(&ctl->next_min[cur]), sc = ld_vol(&ctl->succ[cur]);
+            const int32_t* sr = (const int32_t*)&ctl->succ_range[cur];
+            const int32_t sx = ld_vol(sr), sy = ld_vol(sr + 1);
+            const int32_t c_next = min(nm, sc);
             s_snap[3] = c_next;
             s_snap[4] = ld_vol(&ctl->heavy[cur]);
             s_snap[5] = ld_vol(&ctl->items_last);
             if (c_next != kBig) {
-                const int32_t* r = (const int32_t*)&p.brange[c_next];
-                s_snap[6] = ((long long)ld_vol(r + 1) << 32) | (unsigned)ld_vol(r);
+                if (nm > sc) {
+                    s_snap[6] = ((long long)sy << 32) | (unsigned)sx;
+                } else {
+                    const int32_t* r = (const int32_t*)&p.brange[c_next];
+                    s_snap[6] = ((long long)ld_vol(r + 1) << 32) | (unsigned)ld_vol(r);
+                }
             }
         });
         if (tr) p.trace[round * kTraceWords + 3] = globaltimer();

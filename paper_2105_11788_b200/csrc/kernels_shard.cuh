@@ -115,11 +115,13 @@ __device__ __forceinline__ void shard_merge(const SparseParams& p, int cur, int3
         const int64_t cnt = s_snap[r];
         if (r != p.shard) {
             const int32_t* lst = p.peer_xlist[r] + (int64_t)cur * p.n;
-            for (int64_t i = ((int64_t)tw << 5) + lane; i < cnt; i += (int64_t)tnw << 5) {
-                const int32_t b = lst[i];
+            for (int64_t i0 = (int64_t)tw << 5; i0 < cnt; i0 += (int64_t)tnw << 5) {
+                const int64_t i = i0 + lane;
+                const int32_t b = i < cnt ? lst[i] : 0;
                 const uint32_t bit = 1u << (b & 31);
-                if (!(ld_vol(&p.tblock[b >> 5]) & bit) && !(atomicOr(&p.tblock[b >> 5], bit) & bit))
-                    register_block(p, cur, b);
+                const bool reg = i < cnt && !(ld_vol(&p.tblock[b >> 5]) & bit) &&
+                                 !(atomicOr(&p.tblock[b >> 5], bit) & bit);
+                register_blocks_warp(p, cur, reg, b);
             }
         }
         base += cnt;

@@ -65,7 +65,15 @@ __device__ __forceinline__ void grid_barrier(GridBarrier* gb, unsigned& gen) {
 // never all load the same global words.  solo: the team is this CTA alone.
 template <typename F>
 __device__ __forceinline__ void team_barrier(bool solo, GridBarrier* gb, unsigned& gen, F&& snap) {
+    team_barrier(solo, gb, gen, [] {}, snap);
+}
+
+// ... with pre(): run by warp 0 after the CTA has synchronised and before
+// the CTA arrives (its writes are released with the arrival).
+template <typename G, typename F>
+__device__ __forceinline__ void team_barrier(bool solo, GridBarrier* gb, unsigned& gen, G&& pre, F&& snap) {
     __syncthreads();
+    if (threadIdx.x < 32) pre();
     if (threadIdx.x == 0) {
         if (!solo) {
             const unsigned target = (gen + 1) * gridDim.x;
@@ -88,6 +96,7 @@ struct SCtrl {
     int64_t guard_count;
     int32_t next_min[2];                // min raised label, by round parity
     int32_t succ[2];                    // successor of C in unstable \ {C}
+    int2 succ_range[2];                 // brange of that successor, read in phase A
     int32_t n_small[2];                 // touched blocks of <= 32 members
     int32_t pad1[2];
     unsigned long long big_pack[2];     // (#big touched blocks << 32) | #32-member chunks
@@ -197,35 +206,104 @@ __device__ __forceinline__ void trace_at(const SparseParams& p, int64_t round, i
 
 // ---- hierarchical unstable set --------------------------------------------
 
-// Raise label x.  Fire-and-forget reductions on all three levels (a summary
-// bit may be set redundantly; it only has to be set whenever its range is
-// non-empty).
-__device__ __forceinline__ void u_set(const SparseParams& p, int32_t x) {
-    red_or(&p.U0[x >> 5], 1u << (x & 31));
-    red_or(&p.U1[x >> 15], 1u << ((x >> 10) & 31));
-    red_or(&p.U2[x >> 25], 1u << ((x >> 20) & 31));
+// Phase-B raises are combined per CTA in shared memory and flushed once at
+// the end of the phase (raise_flush): the summary levels U1/U2 have few
+// words (U2 is one word below 32M states) and next_min / splits[round] are
+// single words, so per-raise global reductions from thousands of split
+// blocks serialised in L2 on a handful of addresses.
+constexpr int kU1Smem = 2048;  // U1 words kept per CTA (n <= 2^26); beyond, U1 raises go to global
+__shared__ uint32_t s_u1[kU1Smem];
+__shared__ int32_t s_u1_dirty[kU1Smem];  // U1 words that became non-zero this phase
+__shared__ int32_t s_ndirty;
+__shared__ uint32_t s_u2[32];
+__shared__ int32_t s_nmin;
+__shared__ int32_t s_nsplit;
+
+__device__ __forceinline__ void raise_init() {
+    for (int k = threadIdx.x; k < kU1Smem; k += blockDim.x) s_u1[k] = 0u;
+    if (threadIdx.x < 32) s_u2[threadIdx.x] = 0u;
+    if (threadIdx.x == 0) {
+        s_nmin = 0x7fffffff;
+        s_nsplit = 0;
+        s_ndirty = 0;
+    }
 }
 
-// Clear x (whole warp participates; no concurrent raises in this phase).
-__device__ __forceinline__ void u_clear_warp(const SparseParams& p, int32_t x) {
+// Raise label x: U0 word in global memory, summary bits in the CTA's copy.
+__device__ __forceinline__ void u_set(const SparseParams& p, int32_t x) {
+    red_or(&p.U0[x >> 5], 1u << (x & 31));
+    if (p.nw1 <= kU1Smem) {
+        const int32_t w = x >> 15;
+        if (!atomicOr(&s_u1[w], 1u << ((x >> 10) & 31))) s_u1_dirty[atomicAdd(&s_ndirty, 1)] = w;
+    } else {
+        red_or(&p.U1[x >> 15], 1u << ((x >> 10) & 31));
+    }
+    atomicOr(&s_u2[x >> 25], 1u << ((x >> 20) & 31));
+}
+
+// Warp 0, after a __syncthreads that follows every raise of the phase (the
+// start of team_barrier): publish the CTA's summary bits, raised minimum and
+// split count, and reset them.  Nothing to do for a CTA without a split.
+__device__ __forceinline__ void raise_flush_warp0(const SparseParams& p, int cur, int64_t round) {
     const int lane = threadIdx.x & 31;
-    uint32_t w0 = 0;
-    if (lane == 0) w0 = atomicAnd(&p.U0[x >> 5], ~(1u << (x & 31))) & ~(1u << (x & 31));
-    w0 = __shfl_sync(kFull, w0, 0);
-    if (w0) return;
-    const int32_t c = x >> 10;  // 32-word chunk of U0
+    const int32_t ns = s_nsplit;
+    if (!ns) return;
+    const int32_t nd = s_ndirty;
+    for (int k = lane; k < nd; k += 32) {
+        const int32_t w = s_u1_dirty[k];
+        red_or(&p.U1[w], s_u1[w]);
+        s_u1[w] = 0u;
+    }
+    if (lane < p.nw2) {
+        const uint32_t v = s_u2[lane];
+        if (v) {
+            red_or(&p.U2[lane], v);
+            s_u2[lane] = 0u;
+        }
+    }
+    if (lane == 0) {
+        red_min(&p.ctrl->next_min[cur], s_nmin);
+        if (round < p.splits_cap) red_add(&p.splits[round], ns);
+        s_nmin = 0x7fffffff;
+        s_nsplit = 0;
+        s_ndirty = 0;
+    }
+    __syncwarp();
+}
+
+// Clear C and return its successor: the smallest unstable label > C (kBig
+// if none).  One probe of C's 32-word chunk serves both (whole warp
+// participates; no raises run concurrently in phase A).
+__device__ int32_t u_next_warp(const SparseParams& p, int32_t from);
+__device__ __forceinline__ int32_t u_clear_next_warp(const SparseParams& p, int32_t x) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t bit = 1u << (x & 31);
+    if (lane == 0) red_and(&p.U0[x >> 5], ~bit);
+    const int32_t c = x >> 10;
     const int32_t wi = (c << 5) + lane;
     uint32_t v = wi < p.nw0 ? p.U0[wi] : 0u;
-    if (__ballot_sync(kFull, v != 0u)) return;
-    uint32_t w1 = 0;
-    if (lane == 0) w1 = atomicAnd(&p.U1[c >> 5], ~(1u << (c & 31))) & ~(1u << (c & 31));
-    w1 = __shfl_sync(kFull, w1, 0);
-    if (w1) return;
-    const int32_t d = x >> 20;
-    const int32_t wj = (d << 5) + lane;
-    v = wj < p.nw1 ? p.U1[wj] : 0u;
-    if (__ballot_sync(kFull, v != 0u)) return;
-    if (lane == 0) red_and(&p.U2[d >> 5], ~(1u << (d & 31)));
+    if (wi == (x >> 5)) v &= ~bit;
+    if (!__ballot_sync(kFull, v != 0u)) {  // the chunk is now empty
+        const uint32_t cb = 1u << (c & 31);
+        if (lane == 0) red_and(&p.U1[c >> 5], ~cb);
+        const int32_t d = x >> 20;
+        const int32_t wj = (d << 5) + lane;
+        uint32_t v1 = wj < p.nw1 ? p.U1[wj] : 0u;
+        if (wj == (c >> 5)) v1 &= ~cb;
+        if (!__ballot_sync(kFull, v1 != 0u) && lane == 0) red_and(&p.U2[d >> 5], ~(1u << (d & 31)));
+        return u_next_warp(p, (c + 1) << 10);
+    }
+    // successor inside the chunk: bits above x
+    uint32_t sv = v;
+    if (wi < (x >> 5)) sv = 0u;
+    else if (wi == (x >> 5)) sv = (x & 31) == 31 ? 0u : (v & (~0u << ((x & 31) + 1)));
+    const unsigned b = __ballot_sync(kFull, sv != 0u);
+    if (b) {
+        const int src = __ffs(b) - 1;
+        const int32_t r = (wi << 5) + __ffs(sv) - 1;
+        return __shfl_sync(kFull, r, src);
+    }
+    return u_next_warp(p, (c + 1) << 10);
 }
 
 // Smallest unstable label >= from (kBig if none); whole warp participates.
@@ -279,21 +357,31 @@ __device__ int32_t u_next_warp(const SparseParams& p, int32_t from) {
 
 // ---- phase A helpers --------------------------------------------------------
 
-// Register block b (first touch this round) in the touched lists.
-__device__ __forceinline__ void register_block(const SparseParams& p, int cur, int32_t b) {
+// Register block b (first touch this round) in the touched lists; `reg`
+// lanes of a warp register at once (warp-uniform call): one counter atomic
+// and one `heavy` store per warp instead of one per block -- thousands of
+// blocks are registered per round in the big rounds of c2/c1.
+__device__ __forceinline__ void register_blocks_warp(const SparseParams& p, int cur, bool reg, int32_t b) {
     SCtrl* ctl = p.ctrl;
-    const int2 r = p.brange[b];
-    // leader slot range, loaded alongside the range (phase B then reads it
-    // with the list entry instead of after it)
-    const int32_t ob = p.off ? p.off[b] : b;
-    const int32_t nb = p.off ? p.off[b + 1] - ob : 1;
-    if (r.y > 1) ctl->heavy[cur] = 1;
-    if (r.y <= 32) {
-        const int32_t k = atomicAdd(&ctl->n_small[cur], 1);
-        p.small_list[k] = make_int4(b, r.x, r.y, 0);
-    } else {
-        // two chunk layouts (kernels_big.cuh); each list is ordered by its
-        // own packed counter, so its first-chunk column ascends
+    const int lane = threadIdx.x & 31;
+    int2 r = make_int2(0, 0);
+    int32_t ob = 0, nb = 0;
+    if (reg) {
+        r = p.brange[b];
+        ob = p.off ? p.off[b] : b;
+        nb = p.off ? p.off[b + 1] - ob : 1;
+    }
+    const unsigned heavy = __ballot_sync(kFull, reg && r.y > 1);
+    if (heavy && lane == __ffs(heavy) - 1) ctl->heavy[cur] = 1;
+    const unsigned small = __ballot_sync(kFull, reg && r.y <= 32);
+    if (small) {
+        const int ld = __ffs(small) - 1;
+        int32_t base = 0;
+        if (lane == ld) base = atomicAdd(&ctl->n_small[cur], __popc(small));
+        base = __shfl_sync(kFull, base, ld);
+        if (reg && r.y <= 32) p.small_list[base + __popc(small & lanemask_lt())] = make_int4(b, r.x, r.y, 0);
+    }
+    if (reg && r.y > 32) {
         const int32_t nch1 = (r.y + 31) >> 5, nch4 = (r.y + 32 * kWide - 1) / (32 * kWide);
         const unsigned long long pk =
             atomicAdd(&ctl->big_pack[cur], (1ull << 32) | (unsigned long long)nch1);
@@ -337,16 +425,18 @@ __device__ __forceinline__ bool set_first(uint32_t* bm, int32_t x, bool active) 
 // goes on to the grid-wide test-and-set.
 constexpr int kSeen = 1024;
 
-__device__ __forceinline__ bool cta_first(int32_t* seen, int32_t b) {
+// 0: b already seen by this CTA this round; 1: first insertion; 2: table
+// crowded (the global test-and-set decides).
+__device__ __forceinline__ int cta_first(int32_t* seen, int32_t b) {
     uint32_t h = ((uint32_t)b * 2654435761u) >> 22;  // 10-bit hash
 #pragma unroll 1
     for (int probe = 0; probe < 16; ++probe) {
         const int32_t old = atomicCAS(&seen[h], -1, b);
-        if (old == -1) return true;
-        if (old == b) return false;
+        if (old == -1) return 1;
+        if (old == b) return 0;
         h = (h + 1) & (kSeen - 1);
     }
-    return true;  // table crowded: let the global test-and-set decide
+    return 2;
 }
 
 // ---- phase B helpers --------------------------------------------------------
@@ -399,8 +489,10 @@ __device__ __forceinline__ void raise_split(const SparseParams& p, int cur, int6
         u_set(p, C);
         lo = min(lo, C);
     }
-    red_min(&p.ctrl->next_min[cur], lo);
-    if (round < p.splits_cap) red_add(&p.splits[round], 1);
+    atomicMin(&s_nmin, lo);
+    atomicAdd(&s_nsplit, 1);
+    (void)cur;
+    (void)round;
 }
 
 // A touched block of <= 32 members, finished by one warp.
