@@ -53,6 +53,36 @@ __device__ __forceinline__ int32_t find_owner(const SparseParams& p, int32_t nbi
     return lo + 31 - __clz(b);
 }
 
+// Owner list entry (and leader slot range) of chunk ci.  Up to 64 big blocks
+// the warp loads every entry at once and picks the owner by ballot, one
+// round trip instead of a base search followed by the entry load.
+template <int K>
+__device__ __forceinline__ int32_t find_entry(const SparseParams& p, int32_t nbig, int32_t ci, int4& e, int2& li) {
+    const int lane = threadIdx.x & 31;
+    if (nbig > 64) {
+        const int32_t k = find_owner<K>(p, nbig, ci);
+        e = big_list_of<K>(p)[k];
+        li = big_info_of<K>(p)[k];
+        return k;
+    }
+    const int4* L = big_list_of<K>(p);
+    const int2* I = big_info_of<K>(p);
+    const int4 e0 = lane < nbig ? L[lane] : make_int4(0, 0, 0, 0x7fffffff);
+    const int4 e1 = lane + 32 < nbig ? L[lane + 32] : make_int4(0, 0, 0, 0x7fffffff);
+    const int2 i0 = lane < nbig ? I[lane] : make_int2(0, 0);
+    const int2 i1 = lane + 32 < nbig ? I[lane + 32] : make_int2(0, 0);
+    const unsigned b0 = __ballot_sync(kFull, e0.w <= ci), b1 = __ballot_sync(kFull, e1.w <= ci);
+    const bool hi = b1 != 0u;
+    const int src = 31 - __clz(hi ? b1 : b0);
+    e.x = __shfl_sync(kFull, hi ? e1.x : e0.x, src);
+    e.y = __shfl_sync(kFull, hi ? e1.y : e0.y, src);
+    e.z = __shfl_sync(kFull, hi ? e1.z : e0.z, src);
+    e.w = __shfl_sync(kFull, hi ? e1.w : e0.w, src);
+    li.x = __shfl_sync(kFull, hi ? i1.x : i0.x, src);
+    li.y = __shfl_sync(kFull, hi ? i1.y : i0.y, src);
+    return src + (hi ? 32 : 0);
+}
+
 // A lane's members of a chunk.  Slot base comes with the record; the slot
 // count is the leader's (members share the leader's label set, bcrp.py:16-19).
 template <int K>
@@ -325,8 +355,11 @@ struct OnePassSlot {
     int32_t pad[2];
 };
 
+// Kept members at bs + kbase + rank (from the head of the range), split
+// members at bs + bz - 1 - (sbase + rank) (from its tail): together a
+// permutation of the range whatever the split count.
 template <int K>
-__device__ __forceinline__ void chunk_place(const SparseParams& p, int32_t bs, int32_t keep, int32_t w,
+__device__ __forceinline__ void chunk_place(const SparseParams& p, int32_t bs, int32_t bz, int32_t w,
                                             const ChunkLane<K>& c, const unsigned* bal, const unsigned* kb,
                                             int32_t sbase, int32_t kbase) {
     const int lane = threadIdx.x & 31;
@@ -334,7 +367,7 @@ __device__ __forceinline__ void chunk_place(const SparseParams& p, int32_t bs, i
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         if (c.valid[j]) {
-            const int32_t np = c.sp[j] ? bs + keep + sbase + __popc(bal[j] & lt) : bs + kbase + __popc(kb[j] & lt);
+            const int32_t np = c.sp[j] ? bs + bz - 1 - (sbase + __popc(bal[j] & lt)) : bs + kbase + __popc(kb[j] & lt);
             p.members[np] = c.r[j];
             if (c.sp[j]) p.block[c.r[j].x] = w;
         }
@@ -355,9 +388,9 @@ __device__ int32_t big_onepass_cta(const SparseParams& p, int cur, int64_t round
     unsigned bal[K], kb[K];
     int32_t nsplit = 0, nkeep = 0, wmin = kBig;
     if (has) {
-        k = find_owner<K>(p, nbig, ci);
-        const int4 e = big_list_of<K>(p)[k];
-        const int2 li = big_info_of<K>(p)[k];
+        int4 e;
+        int2 li;
+        k = find_entry<K>(p, nbig, ci, e, li);
         l = e.x;
         bs = e.y;
         bz = e.z;
@@ -397,6 +430,12 @@ __device__ int32_t big_onepass_cta(const SparseParams& p, int cur, int64_t round
         if (nch_b > cnt_cta) {  // the block spans CTAs: combine globally
             if (lane == 0) {
                 if (wid == leader) {
+                    // placement cursors first: kept members fill the range
+                    // from the head, split members from the tail, so the
+                    // bases do not depend on the block's split count and the
+                    // reservation overlaps the arrival wait
+                    const int32_t sb = tot_s ? atomicAdd(&p.scur[l], tot_s) : 0;
+                    const int32_t kbs = tot_k ? atomicAdd(&p.kcur[l], tot_k) : 0;
                     if (tot_s) {
                         red_add(&p.scnt[l], tot_s);
                         red_min(&p.smin[l], mn);
@@ -404,6 +443,8 @@ __device__ int32_t big_onepass_cta(const SparseParams& p, int cur, int64_t round
                     // release: count and minimum are visible before the arrival
                     asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(&p.sarr[l]), "r"(cnt_cta)
                                  : "memory");
+                    slot[wid].sbase = sb;
+                    slot[wid].kbase = kbs;
                 }
                 while (ld_acquire_u32((const unsigned*)&p.sarr[l]) < (unsigned)nch_b) {
                 }
@@ -415,24 +456,19 @@ __device__ int32_t big_onepass_cta(const SparseParams& p, int cur, int64_t round
         } else {
             ns = tot_s;
             w = mn;
+            if (wid == leader && lane == 0) {
+                slot[wid].sbase = 0;
+                slot[wid].kbase = 0;
+            }
         }
         trace_at(p, round, 10);
-        if (ns && wid == leader && lane == 0) {
-            int32_t sb = 0, kbs = 0;
-            if (nch_b > cnt_cta) {
-                if (tot_s) sb = atomicAdd(&p.scur[l], tot_s);
-                if (tot_k) kbs = atomicAdd(&p.kcur[l], tot_k);
-            }
-            slot[wid].sbase = sb;
-            slot[wid].kbase = kbs;
-        }
     }
     __syncthreads();
     trace_at(p, round, 11);
     if (has) {
         if (ns) {
             const int32_t sb = slot[leader].sbase + pre_s, kbs = slot[leader].kbase + pre_k;
-            chunk_place<K>(p, bs, bz - ns, w, c, bal, kb, sb, kbs);
+            chunk_place<K>(p, bs, bz, w, c, bal, kb, sb, kbs);
             if (ci0 == 0 && lane == 0) finish_block(p, cur, round, C, l, bs, bz, ns, w);
         }
         // every chunk of the block has read the leader's marks before anyone

@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
                             reg = true;  // the solo team is this CTA: its table is exact
                         } else if (f) {
                             const uint32_t bit = 1u << (b & 31);
-                            reg = !(ld_vol(&p.tblock[b >> 5]) & bit) && !(atomicOr(&p.tblock[b >> 5], bit) & bit);
+                            reg = !(atomicOr(&p.tblock[b >> 5], bit) & bit);
                         }
                     }
                     register_blocks_warp(p, cur, reg, b);
