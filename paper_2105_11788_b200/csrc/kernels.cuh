@@ -182,7 +182,10 @@ __global__ void k_label_mask(int32_t n, int64_t m, int32_t A, const int32_t* __r
         }
         const LaneRun r = lane_run(addr);
         bits = run_or(bits, r);
-        if (ok && r.rank == 0) atomicOr(&lmask[addr], bits);
+        // fire-and-forget (a 64-bit atomicOr with an unused result still
+        // compiles to a returning ATOMG that stalls the warp)
+        if (ok && r.rank == 0)
+            asm volatile("red.relaxed.gpu.global.or.b64 [%0], %1;" ::"l"(&lmask[addr]), "l"(bits) : "memory");
     }
 }
 

@@ -19,6 +19,7 @@
 constexpr int32_t kSoloMaxC = 64;
 constexpr int32_t kSoloMaxItems = 64;
 constexpr int32_t kSoloSkipSpan = 1024;  // skip-step window of the solo team
+constexpr int kA = 2;                    // in-edges per lane per phase-A step
 
 template <bool IDENT, bool SH>
 __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParams pk) {
@@ -250,51 +251,72 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
                 const int32_t total = __shfl_sync(kFull, incl, 31);
                 const int32_t excl = incl - d;
                 my_edges += (unsigned long long)d;
-                for (int32_t k0 = 0; k0 < total; k0 += 32) {
-                    const int32_t k = k0 + lane;
-                    // owner lane j: the last lane with excl_j <= k
-                    int32_t j = 0;
+                // kA in-edges per lane per step: their loads are issued
+                // together (reverse edges, then source blocks), so a warp
+                // walking a big splitter keeps kA dependent chains in flight
+                for (int32_t k0 = 0; k0 < total; k0 += 32 * kA) {
+                    int32_t s[kA], b[kA];
+                    bool act[kA];
 #pragma unroll
-                    for (int step = 16; step; step >>= 1) {
-                        const int32_t ex = __shfl_sync(kFull, excl, j + step);
-                        if (ex <= k) j += step;
+                    for (int u = 0; u < kA; ++u) {
+                        const int32_t k = k0 + 32 * u + lane;
+                        if (k0 + 32 * u >= total) {  // warp-uniform: nothing left
+                            act[u] = false;
+                            s[u] = -1;
+                            continue;
+                        }
+                        // owner lane j: the last lane with excl_j <= k
+                        int32_t j = 0;
+#pragma unroll
+                        for (int step = 16; step; step >>= 1) {
+                            const int32_t ex = __shfl_sync(kFull, excl, j + step);
+                            if (ex <= k) j += step;
+                        }
+                        const int32_t ej = __shfl_sync(kFull, e0, j);
+                        const int32_t xj = __shfl_sync(kFull, excl, j);
+                        act[u] = k < total;
+                        s[u] = act[u] ? ej + (k - xj) : -1;  // the in-edge index, for now
                     }
-                    const int32_t ej = __shfl_sync(kFull, e0, j);
-                    const int32_t xj = __shfl_sync(kFull, excl, j);
-                    const bool act = k < total;
-                    int32_t s = 0;
-                    if (act) {
-                        const int32_t e = ej + (k - xj);
-                        if (IDENT) {
-                            s = p.rev_src[e];
-                            if (SH) shard_mark(p, cur, s, -1);
-                            else red_or(&p.mark[s >> 5], 1u << (s & 31));
-                        } else {
-                            const int2 r = p.rev[e];
-                            s = r.y;
-                            if (SH) {
-                                shard_mark(p, cur, r.x, s);
+                    int2 rv[kA];
+#pragma unroll
+                    for (int u = 0; u < kA; ++u) {
+                        if (IDENT) rv[u] = make_int2(0, act[u] ? p.rev_src[s[u]] : 0);
+                        else rv[u] = act[u] ? p.rev[s[u]] : make_int2(0, 0);
+                    }
+#pragma unroll
+                    for (int u = 0; u < kA; ++u) {
+                        s[u] = rv[u].y;
+                        if (act[u]) {
+                            if (IDENT) {
+                                if (SH) shard_mark(p, cur, s[u], -1);
+                                else red_or(&p.mark[s[u] >> 5], 1u << (s[u] & 31));
+                            } else if (SH) {
+                                shard_mark(p, cur, rv[u].x, s[u]);
                             } else {
-                                red_or(&p.mark[r.x >> 5], 1u << (r.x & 31));
-                                red_or(&p.touched[s >> 5], 1u << (s & 31));
+                                red_or(&p.mark[rv[u].x >> 5], 1u << (rv[u].x & 31));
+                                red_or(&p.touched[s[u] >> 5], 1u << (s[u] & 31));
                             }
                         }
+                        b[u] = act[u] ? p.block[s[u]] : 0;
                     }
-                    const int32_t b = act ? p.block[s] : 0;
-                    const unsigned same = __match_any_sync(kFull, act ? b : -1 - lane);
-                    const bool rep = act && lane == __ffs(same) - 1;
-                    bool reg = false;
-                    if (rep) {
-                        const int f = cta_first(s_seen, b);
-                        if (f == 1 && solo) {
-                            reg = true;  // the solo team is this CTA: its table is exact
-                        } else if (f) {
-                            const uint32_t bit = 1u << (b & 31);
-                            reg = !(atomicOr(&p.tblock[b >> 5], bit) & bit);
+#pragma unroll
+                    for (int u = 0; u < kA; ++u) {
+                        if (k0 + 32 * u >= total) break;  // warp-uniform
+                        const unsigned same = __match_any_sync(kFull, act[u] ? b[u] : -1 - lane);
+                        const bool rep = act[u] && lane == __ffs(same) - 1;
+                        bool reg = false;
+                        if (rep) {
+                            const int f = cta_first(s_seen, b[u]);
+                            if (f == 1 && solo) {
+                                reg = true;  // the solo team is this CTA: its table is exact
+                            } else if (f) {
+                                const uint32_t bit = 1u << (b[u] & 31);
+                                reg = !(atomicOr(&p.tblock[b[u] >> 5], bit) & bit);
+                            }
                         }
+                        register_blocks_warp(p, cur, reg, b[u]);
+                        if (SH && reg) shard_publish(p, cur, b[u]);
                     }
-                    register_blocks_warp(p, cur, reg, b);
-                    if (SH && reg) shard_publish(p, cur, b);
                 }
             }
         }
