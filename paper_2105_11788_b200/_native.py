@@ -13,7 +13,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbisim.so")
+# BISIM_LIB: developer override (an experimental build of the same library)
+LIB_PATH = os.environ.get("BISIM_LIB") or os.path.join(_HERE, "libbisim.so")
 
 BISIM_OK, BISIM_BAD_INPUT, BISIM_GUARD, BISIM_CUDA, BISIM_ABORTED = 0, 1, 2, 3, 4
 SHARD_VERIFY = 1

@@ -416,7 +416,9 @@ __device__ int32_t big_onepass_cta(const SparseParams& p, int cur, int64_t round
     int32_t leader = wid, cnt_cta = 1, tot_s = nsplit, tot_k = nkeep, pre_s = 0, pre_k = 0, mn = wmin;
     int32_t ns = 0, w = kBig, nch_b = 1;
     if (has) {
-        const OnePassSlot o = slot[lane];  // kSparseThreads / 32 == 32 slots, one per lane
+        OnePassSlot o;  // one slot per warp of the CTA, one per lane
+        if (lane < (int)(blockDim.x >> 5)) o = slot[lane];
+        else o.key = -1;
         const bool same = o.key == k;
         const unsigned msk = __ballot_sync(kFull, same);
         leader = __ffs(msk) - 1;

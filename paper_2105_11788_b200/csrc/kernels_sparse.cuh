@@ -28,7 +28,10 @@
 
 namespace bisim {
 
-constexpr int kSparseThreads = 1024;  // one CTA per SM
+#ifndef BISIM_SPARSE_THREADS
+#define BISIM_SPARSE_THREADS 1024
+#endif
+constexpr int kSparseThreads = BISIM_SPARSE_THREADS;  // one CTA per SM
 constexpr int kMaxShards = 8;         // replicas of the transition-sharded mode
 
 // Grid barrier: one monotonic arrival counter; CTA leaders add with
