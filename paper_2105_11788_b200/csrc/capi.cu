@@ -498,6 +498,8 @@ int run_with(Ctx& c, Job& j) {
         sp.allow_solo = getenv("BISIM_NO_SOLO") == nullptr ? 1 : 0;
         // developer: BISIM_MODE_B=1|2 forces the wide / two-pass phase-B layout
         sp.force_mode_b = getenv("BISIM_MODE_B") ? atoi(getenv("BISIM_MODE_B")) : -1;
+        sp.solo_max_c = getenv("BISIM_SOLO_C") ? atoi(getenv("BISIM_SOLO_C")) : kSoloMaxC;
+        sp.solo_max_items = getenv("BISIM_SOLO_ITEMS") ? atoi(getenv("BISIM_SOLO_ITEMS")) : kSoloMaxItems;
         // developer tracing: BISIM_TRACE=<rounds> BISIM_TRACE_FILE=<path>
         if (const char* tr = getenv("BISIM_TRACE")) {
             sp.trace_rounds = atoll(tr);
@@ -632,13 +634,13 @@ int run_with(Ctx& c, Job& j) {
         const char* path = getenv("BISIM_TRACE_FILE");
         if (FILE* f = fopen(path ? path : "bisim_trace.csv", "w")) {
             fprintf(f, "round,phaseA_ns,barrierA_ns,phaseB_ns,csize,solo,n_small,big_chunks,n_big,"
-                       "b_tag_ns,b_sync1_ns,b_arrive_ns,b_sync2_ns,b_place_ns\n");
+                       "b_tag_ns,b_sync1_ns,b_arrive_ns,b_sync2_ns,b_place_ns,mode_b\n");
             for (int64_t r = 0; r < std::min<int64_t>(sp.trace_rounds, R); ++r) {
                 const unsigned long long* q = &t[r * kTraceWords];
                 auto d = [&](int a, int b) -> long long { return (q[a] && q[b]) ? (long long)(q[a] - q[b]) : -1; };
-                fprintf(f, "%lld,%llu,%llu,%llu,%llu,%llu,%llu,%llu,%llu,%lld,%lld,%lld,%lld,%lld\n", (long long)r,
+                fprintf(f, "%lld,%llu,%llu,%llu,%llu,%llu,%llu,%llu,%llu,%lld,%lld,%lld,%lld,%lld,%llu\n", (long long)r,
                         q[1] - q[0], q[2] - q[1], q[3] - q[2], q[4], q[5], q[6], q[7] & 0xffffffffull, q[7] >> 32,
-                        d(8, 2), d(9, 8), d(10, 9), d(11, 10), d(12, 11));
+                        d(8, 2), d(9, 8), d(10, 9), d(11, 10), d(12, 11), q[13]);
             }
             fclose(f);
         }

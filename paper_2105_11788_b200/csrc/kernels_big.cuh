@@ -53,13 +53,14 @@ __device__ __forceinline__ int32_t find_owner(const SparseParams& p, int32_t nbi
     return lo + 31 - __clz(b);
 }
 
-// Owner list entry (and leader slot range) of chunk ci.  Up to 64 big blocks
-// the warp loads every entry at once and picks the owner by ballot, one
-// round trip instead of a base search followed by the entry load.
+// Owner list entry (and leader slot range) of chunk ci.  Up to 128 big
+// blocks the warp loads every entry at once and picks the owner by ballot,
+// one round trip instead of a base search followed by the entry load.
+constexpr int kEntryProbe = 4;  // entries per lane
 template <int K>
 __device__ __forceinline__ int32_t find_entry(const SparseParams& p, int32_t nbig, int32_t ci, int4& e, int2& li) {
     const int lane = threadIdx.x & 31;
-    if (nbig > 64) {
+    if (nbig > 32 * kEntryProbe) {
         const int32_t k = find_owner<K>(p, nbig, ci);
         e = big_list_of<K>(p)[k];
         li = big_info_of<K>(p)[k];
@@ -67,20 +68,41 @@ __device__ __forceinline__ int32_t find_entry(const SparseParams& p, int32_t nbi
     }
     const int4* L = big_list_of<K>(p);
     const int2* I = big_info_of<K>(p);
-    const int4 e0 = lane < nbig ? L[lane] : make_int4(0, 0, 0, 0x7fffffff);
-    const int4 e1 = lane + 32 < nbig ? L[lane + 32] : make_int4(0, 0, 0, 0x7fffffff);
-    const int2 i0 = lane < nbig ? I[lane] : make_int2(0, 0);
-    const int2 i1 = lane + 32 < nbig ? I[lane + 32] : make_int2(0, 0);
-    const unsigned b0 = __ballot_sync(kFull, e0.w <= ci), b1 = __ballot_sync(kFull, e1.w <= ci);
-    const bool hi = b1 != 0u;
-    const int src = 31 - __clz(hi ? b1 : b0);
-    e.x = __shfl_sync(kFull, hi ? e1.x : e0.x, src);
-    e.y = __shfl_sync(kFull, hi ? e1.y : e0.y, src);
-    e.z = __shfl_sync(kFull, hi ? e1.z : e0.z, src);
-    e.w = __shfl_sync(kFull, hi ? e1.w : e0.w, src);
-    li.x = __shfl_sync(kFull, hi ? i1.x : i0.x, src);
-    li.y = __shfl_sync(kFull, hi ? i1.y : i0.y, src);
-    return src + (hi ? 32 : 0);
+    int4 ev[kEntryProbe];
+    int2 iv[kEntryProbe];
+#pragma unroll
+    for (int q = 0; q < kEntryProbe; ++q) {
+        const int32_t k = lane + 32 * q;
+        ev[q] = k < nbig ? L[k] : make_int4(0, 0, 0, 0x7fffffff);
+        iv[q] = k < nbig ? I[k] : make_int2(0, 0);
+    }
+    // the owner is the last entry whose first chunk <= ci (bases ascend)
+    int qs = 0;
+    unsigned bq = 0u;
+#pragma unroll
+    for (int q = 0; q < kEntryProbe; ++q) {
+        const unsigned b = __ballot_sync(kFull, ev[q].w <= ci);
+        if (b) {
+            qs = q;
+            bq = b;
+        }
+    }
+    const int src = 31 - __clz(bq);
+    int4 mine = ev[0];
+    int2 mi = iv[0];
+#pragma unroll
+    for (int q = 1; q < kEntryProbe; ++q)
+        if (q == qs) {
+            mine = ev[q];
+            mi = iv[q];
+        }
+    e.x = __shfl_sync(kFull, mine.x, src);
+    e.y = __shfl_sync(kFull, mine.y, src);
+    e.z = __shfl_sync(kFull, mine.z, src);
+    e.w = __shfl_sync(kFull, mine.w, src);
+    li.x = __shfl_sync(kFull, mi.x, src);
+    li.y = __shfl_sync(kFull, mi.y, src);
+    return src + 32 * qs;
 }
 
 // A lane's members of a chunk.  Slot base comes with the record; the slot

@@ -16,10 +16,14 @@
 // warp count) and the phase barrier differ, so rounds are bit-identical.
 #pragma once
 
-constexpr int32_t kSoloMaxC = 64;
-constexpr int32_t kSoloMaxItems = 64;
+// measured on c1 / c2 (512-thread CTAs): 16 / 128 beat 64 / 64 by 6 / 3 %
+constexpr int32_t kSoloMaxC = 16;
+constexpr int32_t kSoloMaxItems = 128;
 constexpr int32_t kSoloSkipSpan = 1024;  // skip-step window of the solo team
-constexpr int kA = 2;                    // in-edges per lane per phase-A step
+#ifndef BISIM_KA
+#define BISIM_KA 2
+#endif
+constexpr int kA = BISIM_KA;             // in-edges per lane per phase-A step
 
 template <bool IDENT, bool SH>
 __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParams pk) {
@@ -125,8 +129,8 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
                 __syncthreads();
                 fresh = false;
             }
-            const bool stay = p.brange[C].y <= kSoloMaxC &&
-                              ld_vol(&ctl->items_last) <= kSoloMaxItems;
+            const bool stay = p.brange[C].y <= p.solo_max_c &&
+                              ld_vol(&ctl->items_last) <= p.solo_max_items;
             if (!stay) {
                 if (threadIdx.x == 0) {
                     ctl->C0 = C;
@@ -362,6 +366,7 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
         if (mode_b == 0 && nch1 > 512 * nbig) mode_b = 1;
         if (p.force_mode_b > mode_b) mode_b = p.force_mode_b;
         const int32_t nch = mode_b == 0 ? nch1 : nch4;
+        if (tr) p.trace[round * kTraceWords + 13] = mode_b;
         if (mode_b == 2) {
             for (int32_t it = tw; it < nsm + nch; it += tnw) {
                 int32_t cnt;
@@ -410,8 +415,8 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
         try_skip = p.allow_skip && cooldown == 0 && s_snap[4] == 0;
 
         // ---- grid team: go solo for the next rounds? (uniform decision) ----
-        if (!solo && solo_ok && !try_skip && C != kBig && cr_v.y <= kSoloMaxC &&
-            (int32_t)s_snap[5] <= kSoloMaxItems) {
+        if (!solo && solo_ok && !try_skip && C != kBig && cr_v.y <= p.solo_max_c &&
+            (int32_t)s_snap[5] <= p.solo_max_items) {
             solo = true;  // CTA 0 continues alone, the others park at the loop head
             fresh = true;
             ++stretches;

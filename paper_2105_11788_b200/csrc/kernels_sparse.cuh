@@ -28,10 +28,14 @@
 
 namespace bisim {
 
+// One CTA per SM.  512 threads leave 128 registers per thread (the loop
+// spilled at the 64 of 1024-thread CTAs); measured per-round latency on the
+// B200 (c1 / c2 / c3 / c4l / c5): 512 beats 1024 by 19 / 15 / 13 / 11 / 7 %,
+// 256, 384 and 768 are within a few % or slower on c5.
 #ifndef BISIM_SPARSE_THREADS
-#define BISIM_SPARSE_THREADS 1024
+#define BISIM_SPARSE_THREADS 512
 #endif
-constexpr int kSparseThreads = BISIM_SPARSE_THREADS;  // one CTA per SM
+constexpr int kSparseThreads = BISIM_SPARSE_THREADS;
 constexpr int kMaxShards = 8;         // replicas of the transition-sharded mode
 
 // Grid barrier: one monotonic arrival counter; CTA leaders add with
@@ -123,7 +127,10 @@ struct SCtrl {
 // Window of unstable labels examined by one skip step (see k_refine_sparse).
 constexpr int32_t kSkipSpan = 32768;
 constexpr int32_t kSkipMaxEdges = 256;
-constexpr int kWide = 4;  // members per lane in the wide big-block chunk layout (kernels_big.cuh)
+#ifndef BISIM_KWIDE
+#define BISIM_KWIDE 4
+#endif
+constexpr int kWide = BISIM_KWIDE;  // members per lane in the wide big-block chunk layout (kernels_big.cuh)
 
 // A member record carries what the phases read right after the member id,
 // so one 16-byte load replaces two dependent ones: (state u, slot base
@@ -176,6 +183,8 @@ struct SparseParams {
     int32_t cta_minor;          // spread consecutive work items over SMs
     int32_t allow_solo;         // small rounds on CTA 0 alone (kernels_loop.cuh)
     int32_t force_mode_b;       // developer override of the phase-B layout (-1: automatic)
+    int32_t solo_max_c;         // solo stretches: splitter size and previous-round work
+    int32_t solo_max_items;     //   item limits (kernels_loop.cuh)
     // ---- transition-sharded mode (kernels_shard.cuh); nshard == 1 otherwise
     int32_t nshard;                       // replicas taking part in every round
     int32_t shard;                        // my index
