@@ -68,7 +68,7 @@ struct Ctx {
     int grid_sparse_bcrp = 0, grid_sparse_rcpp = 0;
     std::mutex mu;
     DevBuf src, act, dst, pi0, lmask, off, rev_ptr, cursor, rev_slot, block, nl, mark, unstable,
-        split_list, cmem, splits, ctrl, scan_tmp, rev2, members, bstart, bsize, touched, tblock,
+        split_list, cmem, splits, ctrl, scan_tmp, rev2, members, bstart, bsize, tblock,
         small_list, big_list, big_base, tmp, scnt, smin, kcur, scur, counter, brange, bar, trace, lhash, lkeys,
         lmins, sarr, big_list4, big_base4, big_info, big_info4;
     int launches = 0;
@@ -196,10 +196,10 @@ int64_t loop_bytes(bool bcrp, bool dense, int32_t n, int64_t L, int64_t R, const
         return (R + 1) * per_round + (int64_t)ls.work_edges * 16 + (int64_t)ls.work_splits * 28;
     }
     // per round: C's range and control words; per in-edge of C: the packed
-    // reverse edge, mark and touched read-modify-writes, source block id;
-    // per member of a touched block: member id, touched/mark bits, slot
+    // reverse edge, mark read-modify-write, source block id;
+    // per member of a touched block: member id, mark bits, slot
     // offsets, compaction write and block id write.
-    const int64_t per_edge = bcrp ? 8 + 8 + 8 + 4 : 4 + 8 + 4;
+    const int64_t per_edge = bcrp ? 8 + 8 + 4 : 4 + 8 + 4;
     const int64_t per_member = bcrp ? 4 + 4 + 8 + 4 + 4 + 4 : 4 + 4 + 4 + 4;
     return (R + 1) * 64 + (int64_t)ls.work_edges * per_edge + (int64_t)ls.work_members * per_member;
 }
@@ -448,9 +448,7 @@ int run_with(Ctx& c, Job& j) {
         k_summary<<<grid_for((int64_t)nw1 * 32, TB, c.sms), TB, 0, st>>>(U, nw0, U1, nw1);
         k_summary<<<1, 64, 0, st>>>(U1, nw1, U2, nw2);
         c.launches += 2;
-        uint32_t* touched = (uint32_t*)c.touched.ensure(parities * (nwords + 2) * 4);
         uint32_t* tblock = (uint32_t*)c.tblock.ensure(parities * (nwords + 2) * 4);
-        CK(cudaMemsetAsync(touched, 0, parities * (nwords + 2) * 4, st));
         CK(cudaMemsetAsync(tblock, 0, parities * (nwords + 2) * 4, st));
         sp.n = n;
         sp.A = A;
@@ -467,7 +465,6 @@ int run_with(Ctx& c, Job& j) {
         sp.members = members;
         sp.brange = brange;
         sp.mark = mark;
-        sp.touched = touched;
         sp.tblock = tblock;
         sp.U0 = U;
         sp.U1 = U1;
@@ -498,6 +495,7 @@ int run_with(Ctx& c, Job& j) {
         sp.allow_solo = getenv("BISIM_NO_SOLO") == nullptr ? 1 : 0;
         // developer: BISIM_MODE_B=1|2 forces the wide / two-pass phase-B layout
         sp.force_mode_b = getenv("BISIM_MODE_B") ? atoi(getenv("BISIM_MODE_B")) : -1;
+        sp.pad_exp = getenv("BISIM_EXP") ? atoi(getenv("BISIM_EXP")) : 0;
         sp.solo_max_c = getenv("BISIM_SOLO_C") ? atoi(getenv("BISIM_SOLO_C")) : kSoloMaxC;
         sp.solo_max_items = getenv("BISIM_SOLO_ITEMS") ? atoi(getenv("BISIM_SOLO_ITEMS")) : kSoloMaxItems;
         // developer tracing: BISIM_TRACE=<rounds> BISIM_TRACE_FILE=<path>
@@ -765,7 +763,6 @@ int run_sharded(Job& base, const int32_t* devices, int G, int32_t flags) {
         sp.timeout_ns = 20ull * 1000 * 1000 * 1000;
         for (int r = 0; r < G; ++r) {
             sp.peer_mark[r] = prep[r].sp.mark;
-            sp.peer_touched[r] = prep[r].sp.touched;
             sp.peer_xlist[r] = (int32_t*)S.xlist[r].p;
             sp.peer_xcnt[r] = (int32_t*)S.xcnt[r].p;
             sp.peer_xbar[r] = (unsigned*)S.xbar[r].p;

@@ -106,6 +106,14 @@ __device__ __forceinline__ uint32_t get_bits(const uint32_t* bm, int32_t pos, in
     return len == 32 ? v : (v & ((1u << len) - 1u));
 }
 
+// Any mark among the nr slots starting at pos (a state is "touched" this
+// round iff one of its slots is marked; no separate bitmap is kept).
+__device__ __forceinline__ bool slots_any(const uint32_t* mark, int32_t pos, int32_t nr) {
+    for (int32_t k = 0; k < nr; k += 32)
+        if (get_bits(mark, pos + k, min(32, nr - k))) return true;
+    return false;
+}
+
 // BCRP split test (bcrp.py:260-265) restated per state: s differs from its
 // leader l on some label slot k < nr (same label set => same slot layout).
 __device__ __forceinline__ bool slots_differ(const uint32_t* mark, int32_t os, int32_t ol,

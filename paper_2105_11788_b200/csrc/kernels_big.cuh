@@ -122,8 +122,8 @@ __device__ __forceinline__ int32_t slot_base(const MemberRec& r) {
 }
 
 // Tag a chunk's members.  Loads are staged across the lane's members
-// (records, then touched bits, then mark words) so the K dependency chains
-// overlap instead of running back to back.
+// (records, then mark words) so the K dependency chains overlap instead of
+// running back to back.
 template <bool IDENT, int K>
 __device__ __forceinline__ void chunk_tag(const SparseParams& p, int32_t l, int32_t bs, int32_t bz,
                                           int32_t ci0, int32_t ol, int32_t nrl, ChunkLane<K>& c) {
@@ -146,35 +146,36 @@ __device__ __forceinline__ void chunk_tag(const SparseParams& p, int32_t l, int3
         }
         return;
     }
-    const bool tl = get_bit(p.touched, l);
-    const uint32_t lb = (nrl > 0 && nrl <= 32) ? get_bits(p.mark, ol, nrl) : 0u;
-    uint32_t tw[K], wa[K], wb[K];
+    bool tl;
+    uint32_t lb;
+    leader_marks<IDENT>(p, l, ol, nrl, tl, lb);
+    uint32_t wa[K], wb[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-        // touched word and the member's mark words in one wave of loads;
-        // the mark words are only needed when a mark can differ
-        tw[j] = c.valid[j] ? p.touched[c.r[j].x >> 5] : 0u;
+        // the member's mark words in one wave of loads (they also tell
+        // whether it is touched)
         const int32_t ou = c.r[j].y, w0 = ou >> 5, sh = ou & 31;
-        const bool maybe = c.valid[j] && c.r[j].x != l && nrl > 0 && nrl <= 32;
-        wa[j] = maybe ? p.mark[w0] : 0u;
-        wb[j] = (maybe && sh + nrl > 32) ? p.mark[w0 + 1] : 0u;
+        const bool small = c.valid[j] && nrl > 0 && nrl <= 32;
+        wa[j] = small ? p.mark[w0] : 0u;
+        wb[j] = (small && sh + nrl > 32) ? p.mark[w0 + 1] : 0u;
     }
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-        c.tu[j] = (tw[j] >> (c.r[j].x & 31)) & 1u;
-        const bool need = c.valid[j] && c.r[j].x != l && (c.tu[j] || tl) && nrl > 0;
-        bool sp = false;
-        if (need) {
-            const int32_t ou = c.r[j].y, sh = ou & 31;
+        const int32_t ou = c.r[j].y, sh = ou & 31;
+        bool sp = false, tu = false;
+        if (c.valid[j] && nrl > 0) {
             if (nrl <= 32) {
                 uint32_t v = wa[j] >> sh;
                 if (sh + nrl > 32) v |= wb[j] << (32 - sh);
                 if (nrl < 32) v &= (1u << nrl) - 1u;
-                sp = v != lb;
+                tu = v != 0u;
+                sp = c.r[j].x != l && v != lb;
             } else {
-                sp = slots_differ(p.mark, ou, ol, nrl);
+                tu = slots_any(p.mark, ou, nrl);
+                sp = c.r[j].x != l && (tu || tl) && slots_differ(p.mark, ou, ol, nrl);
             }
         }
+        c.tu[j] = tu;
         c.sp[j] = sp;
     }
 }
@@ -258,6 +259,7 @@ __device__ int32_t big_tag(const SparseParams& p, int32_t nbig, int32_t ci) {
         if (!c.valid[j]) continue;
         MemberRec t = c.r[j];
         if (c.sp[j]) t.x = -1 - t.x;
+        if (c.tu[j]) t.y |= (int32_t)0x80000000;  // touched: clear its marks in sub-phase 2
         p.tmp[bs + ci0 + 32 * j + lane] = t;
     }
     unsigned bal[K], kb[K];
@@ -280,7 +282,6 @@ __device__ void big_split(const SparseParams& p, int cur, int64_t round, int32_t
     const int32_t l = e.x, bs = e.y, bz = e.z, ci0 = (ci - e.w) * (32 * K);
     const int32_t nrl = big_info_of<K>(p)[k].y;
     ChunkLane<K> c;
-    uint32_t tw[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         const int32_t i = ci0 + 32 * j + lane;
@@ -288,11 +289,10 @@ __device__ void big_split(const SparseParams& p, int cur, int64_t round, int32_t
         MemberRec t = c.valid[j] ? p.tmp[bs + i] : make_int4(0, 0, 0, 0);
         c.sp[j] = c.valid[j] && t.x < 0;
         if (c.sp[j]) t.x = -1 - t.x;
+        c.tu[j] = c.valid[j] && t.y < 0;
+        t.y &= 0x7fffffff;
         c.r[j] = t;
     }
-#pragma unroll
-    for (int j = 0; j < K; ++j)
-        tw[j] = c.valid[j] ? (IDENT ? p.mark[c.r[j].x >> 5] : p.touched[c.r[j].x >> 5]) : 0u;
     const int32_t ns = p.scnt[l];
     if (ns) {
         unsigned bal[K], kb[K];
@@ -303,11 +303,8 @@ __device__ void big_split(const SparseParams& p, int cur, int64_t round, int32_t
         if (ci0 == 0 && lane == 0) finish_block(p, cur, round, C, l, bs, bz, ns, w);
     }
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-        if (!c.valid[j]) continue;
-        const bool tu = (tw[j] >> (c.r[j].x & 31)) & 1u;
-        clear_member<IDENT>(p, c.r[j].x, tu, slot_base<IDENT>(c.r[j]), nrl);
-    }
+    for (int j = 0; j < K; ++j)
+        if (c.valid[j]) clear_member<IDENT>(p, c.r[j].x, c.tu[j], slot_base<IDENT>(c.r[j]), nrl);
     if (ci0 == 0 && lane == 0) red_and(&p.tblock[l >> 5], ~(1u << (l & 31)));
 }
 

@@ -284,21 +284,22 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
                     int2 rv[kA];
 #pragma unroll
                     for (int u = 0; u < kA; ++u) {
-                        if (IDENT) rv[u] = make_int2(0, act[u] ? p.rev_src[s[u]] : 0);
-                        else rv[u] = act[u] ? p.rev[s[u]] : make_int2(0, 0);
+                        // reverse edges stream through (evict-first), so they do not push
+                        // the randomly accessed per-state arrays out of L2
+                        if (IDENT) rv[u] = make_int2(0, act[u] ? __ldcs(&p.rev_src[s[u]]) : 0);
+                        else rv[u] = act[u] ? (p.pad_exp == 2 ? p.rev[s[u]] : __ldcs(&p.rev[s[u]])) : make_int2(0, 0);
                     }
 #pragma unroll
                     for (int u = 0; u < kA; ++u) {
                         s[u] = rv[u].y;
                         if (act[u]) {
                             if (IDENT) {
-                                if (SH) shard_mark(p, cur, s[u], -1);
+                                if (SH) shard_mark(p, cur, s[u]);
                                 else red_or(&p.mark[s[u] >> 5], 1u << (s[u] & 31));
                             } else if (SH) {
-                                shard_mark(p, cur, rv[u].x, s[u]);
+                                shard_mark(p, cur, rv[u].x);
                             } else {
                                 red_or(&p.mark[rv[u].x >> 5], 1u << (rv[u].x & 31));
-                                red_or(&p.touched[s[u] >> 5], 1u << (s[u] & 31));
                             }
                         }
                         b[u] = act[u] ? p.block[s[u]] : 0;

@@ -5,7 +5,7 @@
 // Every replica holds the whole partition state (block, members, ranges,
 // unstable set) and runs the same rounds; only phase A's transition scan is
 // divided: replica g walks the in-edges of C whose source lies in its range.
-// Mark and touched bits go to EVERY replica's buffers (fire-and-forget
+// Mark bits go to EVERY replica's buffers (fire-and-forget
 // reductions over NVLink peer memory -- the paper's per-round mark-bitmap
 // OR-reduction, done inside the persistent kernel instead of by a
 // collective), and the touched blocks each replica registered first are
@@ -15,7 +15,7 @@
 // published and runs phase B on its own copy.  Phase B is a deterministic
 // function of (partition, marks), so the replicas stay identical.
 //
-// Round state written by remote replicas (marks, touched bits, published
+// Round state written by remote replicas (marks, published
 // lists) is double-buffered by round parity: a replica cannot reach round
 // r + 2 before every replica has finished round r, so buffers of parity r & 1
 // are only cleared and reused when nobody reads them.
@@ -35,18 +35,14 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
 
 __device__ __forceinline__ void shard_select_parity(SparseParams& pl, const SparseParams& pk, int cur) {
     pl.mark = pk.mark + cur * pk.mark_stride;
-    pl.touched = pk.touched + cur * pk.bm_stride;
     pl.tblock = pk.tblock + cur * pk.bm_stride;
 }
 
-// Mark slot `slot` (and touched state s >= 0) in every replica.
-__device__ __forceinline__ void shard_mark(const SparseParams& p, int cur, int32_t slot, int32_t s) {
-    const int64_t mo = cur * p.mark_stride + (slot >> 5), to = cur * p.bm_stride + (s >> 5);
-    const uint32_t mb = 1u << (slot & 31), tb = 1u << (s & 31);
-    for (int r = 0; r < p.nshard; ++r) {
-        red_or(p.peer_mark[r] + mo, mb);
-        if (s >= 0) red_or(p.peer_touched[r] + to, tb);
-    }
+// Mark slot `slot` in every replica.
+__device__ __forceinline__ void shard_mark(const SparseParams& p, int cur, int32_t slot) {
+    const int64_t mo = cur * p.mark_stride + (slot >> 5);
+    const uint32_t mb = 1u << (slot & 31);
+    for (int r = 0; r < p.nshard; ++r) red_or(p.peer_mark[r] + mo, mb);
 }
 
 // This replica registered block b first (locally): publish it.

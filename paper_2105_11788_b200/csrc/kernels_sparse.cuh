@@ -7,7 +7,7 @@
 //            the state permutation grouped by block -- mark the slots of
 //            their in-edges (reverse CSR).  In-edges are spread over the
 //            lanes of a warp (a warp scan of the members' in-degrees), mark
-//            and touched bits are fire-and-forget reductions, and each source
+//            bits are fire-and-forget reductions, and each source
 //            block is registered once in the touched-block lists.  One warp
 //            clears C in the hierarchical unstable set and finds C's
 //            successor meanwhile.
@@ -154,14 +154,13 @@ struct SparseParams {
     int4* members;      // member records grouped by block (see MemberRec)
     int2* brange;       // (start, size) of block `label` in members (valid for leaders)
     uint32_t* mark;     // L-bit mark bitmap
-    uint32_t* touched;  // n-bit: state has a marked slot this round (BCRP)
     uint32_t* tblock;   // n-bit: block label registered this round
     uint32_t* U0;       // unstable labels, 3-level summary (1 bit per 1024 / 1M)
     uint32_t* U1;
     uint32_t* U2;
     int32_t nw0, nw1, nw2;
     int32_t pad;
-    int4* small_list;     // touched blocks of <= 32 members: (label, start, size, -)
+    int4* small_list;     // touched blocks of <= 32 members: (label, start, size | nrl << 6, leader slot base)
     int4* big_list;       // larger touched blocks: (label, start, size, first chunk)
     int32_t* big_base;    // first chunk of each big touched block (ascending)
     int4* big_list4;      // the same blocks in the kWide chunk layout
@@ -185,13 +184,13 @@ struct SparseParams {
     int32_t force_mode_b;       // developer override of the phase-B layout (-1: automatic)
     int32_t solo_max_c;         // solo stretches: splitter size and previous-round work
     int32_t solo_max_items;     //   item limits (kernels_loop.cuh)
+    int32_t pad_exp;            // developer experiment switch (BISIM_EXP)
     // ---- transition-sharded mode (kernels_shard.cuh); nshard == 1 otherwise
     int32_t nshard;                       // replicas taking part in every round
     int32_t shard;                        // my index
     int64_t mark_stride;                  // words from the parity-0 to the parity-1 mark buffer
-    int64_t bm_stride;                    // same for the touched / tblock bitmaps
-    uint32_t* peer_mark[kMaxShards];      // every replica's mark / touched buffers (parity 0)
-    uint32_t* peer_touched[kMaxShards];
+    int64_t bm_stride;                    // same for the tblock bitmap
+    uint32_t* peer_mark[kMaxShards];      // every replica's mark buffer (parity 0)
     int32_t* xlist;                       // [2][n] blocks this replica registered first, by parity
     int32_t* peer_xlist[kMaxShards];
     int32_t* peer_xcnt[kMaxShards];       // [2] lengths of those lists
@@ -391,7 +390,9 @@ __device__ __forceinline__ void register_blocks_warp(const SparseParams& p, int 
         int32_t base = 0;
         if (lane == ld) base = atomicAdd(&ctl->n_small[cur], __popc(small));
         base = __shfl_sync(kFull, base, ld);
-        if (reg && r.y <= 32) p.small_list[base + __popc(small & lanemask_lt())] = make_int4(b, r.x, r.y, 0);
+        // (label, start, size | leader slot count << 6, leader slot base)
+        if (reg && r.y <= 32)
+            p.small_list[base + __popc(small & lanemask_lt())] = make_int4(b, r.x, r.y | (nb << 6), ob);
     }
     if (reg && r.y > 32) {
         const int32_t nch1 = (r.y + 31) >> 5, nch4 = (r.y + 32 * kWide - 1) / (32 * kWide);
@@ -456,9 +457,11 @@ __device__ __forceinline__ int cta_first(int32_t* seen, int32_t b) {
 // Split test of member record r against its leader l (slot base ol, nrl
 // slots: members share the leader's label set, hence its slot count,
 // bcrp.py:16-19).
+// tu: u has a marked slot this round; lb: the leader's slot bits (nrl <= 32).
 template <bool IDENT>
 __device__ __forceinline__ bool member_splits(const SparseParams& p, MemberRec r, int32_t l, bool tl,
-                                              int32_t ol, int32_t nrl, bool& tu, int32_t& ou, int32_t& nr) {
+                                              uint32_t lb, int32_t ol, int32_t nrl, bool& tu, int32_t& ou,
+                                              int32_t& nr) {
     const int32_t u = r.x;
     if (IDENT) {
         tu = get_bit(p.mark, u);
@@ -466,11 +469,33 @@ __device__ __forceinline__ bool member_splits(const SparseParams& p, MemberRec r
         nr = 1;
         return u != l && (tu != tl);
     }
-    tu = get_bit(p.touched, u);
     ou = r.y;
     nr = nrl;
-    if (u == l || !(tu || tl) || nr == 0) return false;
+    if (nr == 0) {
+        tu = false;
+        return false;
+    }
+    if (nr <= 32) {
+        const uint32_t ub = get_bits(p.mark, ou, nr);
+        tu = ub != 0u;
+        return u != l && ub != lb;
+    }
+    tu = slots_any(p.mark, ou, nr);
+    if (u == l || !(tu || tl)) return false;
     return slots_differ(p.mark, ou, ol, nr);
+}
+
+// Leader marks of a BCRP block: lb = its slot bits when nrl <= 32, tl = any.
+template <bool IDENT>
+__device__ __forceinline__ void leader_marks(const SparseParams& p, int32_t l, int32_t ol, int32_t nrl, bool& tl,
+                                             uint32_t& lb) {
+    if (IDENT) {
+        tl = get_bit(p.mark, l);
+        lb = tl ? 1u : 0u;
+        return;
+    }
+    lb = (nrl > 0 && nrl <= 32) ? get_bits(p.mark, ol, nrl) : 0u;
+    tl = nrl <= 32 ? lb != 0u : slots_any(p.mark, ol, nrl);
 }
 
 template <bool IDENT>
@@ -481,7 +506,6 @@ __device__ __forceinline__ void clear_member(const SparseParams& p, int32_t u, b
         red_and(&p.mark[u >> 5], ~(1u << (u & 31)));
         return;
     }
-    red_and(&p.touched[u >> 5], ~(1u << (u & 31)));
     int32_t pos = ou, left = nr;
     while (left > 0) {
         const int32_t sh = pos & 31, len = min(left, 32 - sh);
@@ -511,15 +535,18 @@ __device__ __forceinline__ void raise_split(const SparseParams& p, int cur, int6
 template <bool IDENT>
 __device__ int32_t process_small(const SparseParams& p, int cur, int64_t round, int32_t C, int4 e) {
     const int lane = threadIdx.x & 31;
-    const int32_t l = e.x, bs = e.y, bz = e.z;
+    const int32_t l = e.x, bs = e.y, bz = e.z & 63;
     const bool valid = lane < bz;
     const MemberRec rec = valid ? p.members[bs + lane] : make_int4(-1, 0, 0, 0);
     const int32_t u = rec.x;
-    const bool tl = IDENT ? get_bit(p.mark, l) : get_bit(p.touched, l);
-    const int32_t ol = IDENT ? l : p.off[l], nrl = IDENT ? 1 : p.off[l + 1] - ol;
+    // the leader's slot range came with the list entry (register_blocks_warp)
+    const int32_t ol = IDENT ? l : e.w, nrl = IDENT ? 1 : (e.z >> 6);
+    bool tl;
+    uint32_t lb;
+    leader_marks<IDENT>(p, l, ol, nrl, tl, lb);
     bool tu = false;
     int32_t ou = 0, nr = 0;
-    const bool sp = valid && member_splits<IDENT>(p, rec, l, tl, ol, nrl, tu, ou, nr);
+    const bool sp = valid && member_splits<IDENT>(p, rec, l, tl, lb, ol, nrl, tu, ou, nr);
     const unsigned bal = __ballot_sync(kFull, sp);
     if (bal) {
         const int32_t ns = __popc(bal);
