@@ -308,52 +308,6 @@ __device__ void big_split(const SparseParams& p, int cur, int64_t round, int32_t
     if (ci0 == 0 && lane == 0) red_and(&p.tblock[l >> 5], ~(1u << (l & 31)));
 }
 
-// one pass (every item on its own warp)
-template <bool IDENT, int K>
-__device__ int32_t big_onepass(const SparseParams& p, int cur, int64_t round, int32_t C, int32_t nbig,
-                               int32_t ci) {
-    const int lane = threadIdx.x & 31;
-    const int32_t k = find_owner<K>(p, nbig, ci);
-    const int4 e = big_list_of<K>(p)[k];
-    const int2 li = big_info_of<K>(p)[k];
-    const int32_t l = e.x, bs = e.y, bz = e.z, ci0 = (ci - e.w) * (32 * K);
-    const int32_t ol = li.x, nrl = li.y;
-    ChunkLane<K> c;
-    chunk_tag<IDENT, K>(p, l, bs, bz, ci0, ol, nrl, c);
-    unsigned bal[K], kb[K];
-    int32_t nsplit, nkeep, wmin;
-    chunk_counts<K>(c, bal, kb, nsplit, nkeep, wmin);
-    const int32_t nch_b = (bz + 32 * K - 1) / (32 * K);
-    int32_t ns = nsplit, w = wmin;
-    if (nch_b > 1) {
-        if (lane == 0) {
-            if (nsplit) {
-                red_add(&p.scnt[l], nsplit);
-                red_min(&p.smin[l], wmin);
-            }
-            // release: the count/minimum above are visible before the arrival
-            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(&p.sarr[l]) : "memory");
-            while (ld_acquire_u32((const unsigned*)&p.sarr[l]) < (unsigned)nch_b) {
-            }
-            ns = ld_vol(&p.scnt[l]);
-            w = ld_vol(&p.smin[l]);
-        }
-        ns = __shfl_sync(kFull, ns, 0);
-        w = __shfl_sync(kFull, w, 0);
-    }
-    if (ns) {
-        chunk_compact<K>(p, l, bs, bz, ns, w, c, bal, kb, nsplit, nkeep);
-        if (ci0 == 0 && lane == 0) finish_block(p, cur, round, C, l, bs, bz, ns, w);
-    }
-    // every chunk has read the leader's marks before anyone clears: the
-    // arrival count above is complete (or the block is a single chunk)
-#pragma unroll
-    for (int j = 0; j < K; ++j)
-        if (c.valid[j]) clear_member<IDENT>(p, c.r[j].x, c.tu[j], slot_base<IDENT>(c.r[j]), nrl);
-    if (ci0 == 0 && lane == 0) red_and(&p.tblock[l >> 5], ~(1u << (l & 31)));
-    return min(32 * K, bz - ci0);
-}
-
 // ---- one pass with CTA-level aggregation ----------------------------------
 //
 // Every warp of the CTA calls this once per round (ci < 0: no big chunk).

@@ -235,9 +235,15 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
         {
             const int2 cr = cr_c == C ? cr_v : p.brange[C];
             const int32_t cs = cr.x, cz = cr.y;
-            // members per warp: spread small splitters one member per warp so
-            // their in-edges are walked by as many warps as possible
-            const int32_t g = cz >= tnw * 32 ? 32 : max(1, (cz + tnw - 1) / tnw);
+            // members per warp and iteration: every warp gets the same number
+            // of iterations (the smallest that keeps g <= 32), so no warp
+            // walks a second slice while most idle; small splitters get one
+            // member per warp, their in-edges walked by as many warps as possible
+            int32_t g = max(1, (cz + tnw - 1) / tnw);  // 32-bit: cz < 2^30, tnw < 2^13
+            if (g > 32) {
+                const int32_t iters = (cz + tnw * 32 - 1) / (tnw * 32);
+                g = (cz + iters * tnw - 1) / (iters * tnw);
+            }
             for (int64_t i0 = (int64_t)tw * g; i0 < cz; i0 += (int64_t)tnw * g) {
                 const int64_t i = i0 + lane;
                 int32_t e0 = 0, d = 0;
