@@ -70,7 +70,7 @@ struct Ctx {
     DevBuf src, act, dst, pi0, lmask, off, rev_ptr, cursor, rev_slot, block, nl, mark, unstable,
         split_list, cmem, splits, ctrl, scan_tmp, rev2, members, bstart, bsize, tblock,
         small_list, big_list, big_base, tmp, scnt, smin, kcur, scur, counter, brange, bar, trace, lhash, lkeys,
-        lmins, sarr, big_list4, big_base4, big_info, big_info4;
+        lmins, sarr, big_list4, big_base4, big_info, big_info4, sinfo;
     int launches = 0;
 };
 
@@ -324,12 +324,19 @@ int run_with(Ctx& c, Job& j) {
             k_rev_fill<true><<<g, TB, 0, st>>>(n, m, d_src, d_act, d_dst, lmask, off, cursor, rev_slot);
         else if (dense)
             k_rev_fill<false><<<g, TB, 0, st>>>(n, m, d_src, d_act, d_dst, lmask, off, cursor, rev_slot);
-        else if (j.bcrp)
+        else if (j.bcrp) {
+            int4* sinfo = nullptr;
+            if (W == 1) {
+                sinfo = (int4*)c.sinfo.ensure((int64_t)n * 16);
+                k_pack_sinfo<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, lmask, off, sinfo);
+                ++c.launches;
+            }
             k_rev_fill2<true><<<g, TB, 0, st>>>(n, m, d_src, d_act, d_dst, lmask, off, cursor, rev2, nullptr,
-                                                src_lo, src_hi);
-        else
+                                                src_lo, src_hi, sinfo);
+        } else {
             k_rev_fill2<false><<<g, TB, 0, st>>>(n, m, d_src, d_act, d_dst, lmask, off, cursor, nullptr, rev_src,
-                                                 src_lo, src_hi);
+                                                 src_lo, src_hi, nullptr);
+        }
         ++c.launches;
     }
     CK(cudaGetLastError());

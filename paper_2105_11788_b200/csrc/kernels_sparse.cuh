@@ -667,12 +667,23 @@ __global__ void k_summary(const uint32_t* __restrict__ lo, int32_t nlo, uint32_t
     }
 }
 
+// (label mask, slot base) of every state in one 16-byte record, so the
+// reverse fill's random lookup by source costs one sector, not two (W == 1).
+__global__ void k_pack_sinfo(int32_t n, const unsigned long long* __restrict__ lmask,
+                             const int32_t* __restrict__ off, int4* sinfo) {
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long w = lmask[s];
+        sinfo[s] = make_int4((int32_t)(w & 0xffffffffull), (int32_t)(w >> 32), off[s], 0);
+    }
+}
+
 // Pack BCRP reverse edges (slot, source) for one 8-byte load per in-edge.
 template <bool BCRP>
 __global__ void k_rev_fill2(int32_t n, int64_t m, const int32_t* __restrict__ src,
                             const int32_t* __restrict__ act, const int32_t* __restrict__ dst,
                             const unsigned long long* __restrict__ lmask, const int32_t* __restrict__ off,
-                            int32_t* cursor, int2* rev, int32_t* rev_src, int32_t lo, int32_t hi) {
+                            int32_t* cursor, int2* rev, int32_t* rev_src, int32_t lo, int32_t hi,
+                            const int4* __restrict__ sinfo) {
     // only transitions with source in [lo, hi) (the whole range unless sharded)
     const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -686,7 +697,15 @@ __global__ void k_rev_fill2(int32_t n, int64_t m, const int32_t* __restrict__ sr
         }
         if (in) {
             t = dst[i];
-            slot = BCRP ? off[s] + label_rank(lmask, n, s, act[i]) : s;
+            if (!BCRP) {
+                slot = s;
+            } else if (sinfo) {
+                const int4 q = sinfo[s];
+                const unsigned long long w = ((unsigned long long)(uint32_t)q.y << 32) | (uint32_t)q.x;
+                slot = q.z + __popcll(w & ((1ull << (act[i] & 63)) - 1ull));
+            } else {
+                slot = off[s] + label_rank(lmask, n, s, act[i]);
+            }
         }
         const LaneRun run = lane_run(t);
         int32_t base = 0;

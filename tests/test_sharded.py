@@ -19,7 +19,7 @@ from paper_2105_11788_b200.sharded import bcrp_sharded_arrays, rcpp_sharded_arra
 
 pytestmark = pytest.mark.gpu
 
-SHARDS = [[0, 0], [0, 0, 0], [0, 0, 0, 0]]
+SHARDS = [[0], [0, 0], [0, 0, 0], [0, 0, 0, 0]]
 
 
 def _same(block, st, exp, what):
