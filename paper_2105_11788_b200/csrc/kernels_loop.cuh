@@ -235,6 +235,7 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
         {
             const int2 cr = cr_c == C ? cr_v : p.brange[C];
             const int32_t cs = cr.x, cz = cr.y;
+            const bool batch = !solo && cz >= p.batch_min_c;  // CTA-uniform
             // members per warp and iteration: every warp gets the same number
             // of iterations (the smallest that keeps g <= 32), so no warp
             // walks a second slice while most idle; small splitters get one
@@ -320,13 +321,34 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
                             const int f = cta_first(s_seen, b[u]);
                             if (f == 1 && solo) {
                                 reg = true;  // the solo team is this CTA: its table is exact
-                            } else if (f) {
+                            } else if (f == 2 || (f == 1 && !batch)) {
                                 const uint32_t bit = 1u << (b[u] & 31);
                                 reg = !(atomicOr(&p.tblock[b[u] >> 5], bit) & bit);
                             }
                         }
-                        register_blocks_warp(p, cur, reg, b[u]);
-                        if (SH && reg) shard_publish(p, cur, b[u]);
+                        if (__any_sync(kFull, reg)) {
+                            register_blocks_warp(p, cur, reg, b[u]);
+                            if (SH && reg) shard_publish(p, cur, b[u]);
+                        }
+                    }
+                }
+            }
+            if (batch) {
+                // a huge splitter: the CTA's table holds every source block
+                // its warps met; one wave of global test-and-sets registers
+                // them, instead of a returning atomic inside the walk's steps
+                __syncthreads();
+                for (int k0 = 0; k0 < kSeen; k0 += blockDim.x) {
+                    const int k = k0 + threadIdx.x;
+                    const int32_t b = s_seen[k];
+                    bool reg = false;
+                    if (b >= 0) {
+                        const uint32_t bit = 1u << (b & 31);
+                        reg = !(atomicOr(&p.tblock[b >> 5], bit) & bit);
+                    }
+                    if (__any_sync(kFull, reg)) {
+                        register_blocks_warp(p, cur, reg, b);
+                        if (SH && reg) shard_publish(p, cur, b);
                     }
                 }
             }

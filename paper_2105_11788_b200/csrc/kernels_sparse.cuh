@@ -185,6 +185,7 @@ struct SparseParams {
     int32_t solo_max_c;         // solo stretches: splitter size and previous-round work
     int32_t solo_max_items;     //   item limits (kernels_loop.cuh)
     int32_t pad_exp;            // developer experiment switch (BISIM_EXP)
+    int32_t batch_min_c;        // splitter size from which phase A registers blocks in one wave
     // ---- transition-sharded mode (kernels_shard.cuh); nshard == 1 otherwise
     int32_t nshard;                       // replicas taking part in every round
     int32_t shard;                        // my index
@@ -436,7 +437,7 @@ __device__ __forceinline__ bool set_first(uint32_t* bm, int32_t x, bool active) 
 // C usually share few source blocks, and thousands of warps hammering the
 // same tblock words serialise in L2.  Only the first inserter of b in a CTA
 // goes on to the grid-wide test-and-set.
-constexpr int kSeen = 1024;
+constexpr int kSeen = 1024;  // a multiple of the CTA size
 
 // 0: b already seen by this CTA this round; 1: first insertion; 2: table
 // crowded (the global test-and-set decides).
