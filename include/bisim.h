@@ -172,6 +172,14 @@ int bisim_is_stable(int32_t n, int64_t m, int32_t num_actions, const int32_t *sr
                     const int32_t *act, const int32_t *dst, const int32_t *block,
                     int32_t *stable_out, int device);
 
+/* is_stable_under(lts, partition, states) (oracle.py:144-154): *stable_out = 1
+ * iff every state reaches the set `states` (num_states ids; ids outside
+ * 0..n-1 are never reached) via the same actions as its leader. */
+int bisim_is_stable_under(int32_t n, int64_t m, int32_t num_actions, const int32_t *src,
+                          const int32_t *act, const int32_t *dst, const int32_t *block,
+                          const int32_t *states, int64_t num_states, int32_t *stable_out,
+                          int device);
+
 /* partition_from_assignment(assignment) (lts.py:117-128): states sharing an
  * id share a block, whose leader is its smallest state. */
 int bisim_canonical(int32_t n, const int64_t *assignment, int32_t *block_out, int device);

@@ -261,6 +261,7 @@ def post(count=400):
     a random one), plus random id assignments."""
     pb = _ref()
     from parbisim.oracle import is_stable as ref_is_stable
+    from parbisim.oracle import is_stable_under as ref_is_stable_under
     with gzip.open(os.path.join(OUT, "sweep.json.gz"), "rt") as fh:
         sweep_recs = json.load(fh)[:count]
     with gzip.open(os.path.join(OUT, "cases.json.gz"), "rt") as fh:
@@ -284,7 +285,11 @@ def post(count=400):
         for name, blk in parts.items():
             p = pb.Partition(blk)
             q = pb.quotient(lts, p)
+            subsets = [sorted(rng.sample(range(n), rng.randint(0, n))) for _ in range(2)]
+            # one block of the partition as the target set (the splitter case)
+            subsets.append([t for t in range(n) if blk[t] == blk[rng.randrange(n)]])
             res[name] = {"block": blk, "stable": ref_is_stable(lts, p),
+                         "under": [[sub, ref_is_stable_under(lts, p, sub)] for sub in subsets],
                          "q_n": q.n, "q_initial": q.initial_state,
                          "q_src": [t.source for t in q.transitions],
                          "q_act": [t.action for t in q.transitions],

@@ -7,6 +7,7 @@ tests/test_oracle_golden.py).
 
     quotient            /root/reference/pkg/src/parbisim/aut.py:132-152
     is_stable           /root/reference/pkg/src/parbisim/oracle.py:128-141
+    is_stable_under     /root/reference/pkg/src/parbisim/oracle.py:144-154
     canonical           /root/reference/pkg/src/parbisim/lts.py:117-128
 
 numpy restatements of the same set algebra (first occurrences via
@@ -60,6 +61,23 @@ def is_stable(n, src, act, dst, block):
     # sig(s) within sig(block[s]); equal sizes then give equality
     lead = _keys(block[s], a, b)
     return bool(np.all(np.isin(lead, sig)))
+
+
+def is_stable_under(n, src, act, dst, block, states):
+    """oracle.py:144-154: reach[s] = {a : s -a-> t, t in states}; stable iff
+    reach[s] == reach[block[s]] for every s."""
+    block = np.asarray(block, np.int64)
+    src, act, dst = (np.asarray(x, np.int64) for x in (src, act, dst))
+    target = np.zeros(n, bool)
+    st = np.asarray(list(states), np.int64)
+    target[st[(st >= 0) & (st < n)]] = True
+    sel = target[dst] if dst.size else np.zeros(0, bool)
+    pairs = np.unique(_keys(src[sel], act[sel])) if sel.any() else _keys([], [])
+    s_, a_ = pairs["f0"], pairs["f1"]
+    cnt = np.bincount(s_, minlength=n)
+    if np.any(cnt != cnt[block]):
+        return False
+    return bool(np.all(np.isin(_keys(block[s_], a_), pairs)))
 
 
 def canonical(assignment):

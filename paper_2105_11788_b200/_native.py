@@ -76,7 +76,7 @@ EXPORTS = ("bisim_bcrp", "bisim_rcpp", "bisim_bcrp_ex", "bisim_rcpp_ex", "bisim_
            "bisim_device_count", "bisim_stream", "bisim_version", "bisim_quotient",
            "bisim_is_stable", "bisim_canonical", "bisim_aut_parse", "bisim_aut_read_file",
            "bisim_aut_columns", "bisim_aut_label", "bisim_aut_free", "bisim_bcrp_sharded",
-           "bisim_rcpp_sharded")
+           "bisim_rcpp_sharded", "bisim_is_stable_under")
 
 
 def lib():
@@ -113,6 +113,8 @@ def lib():
             L.bisim_is_stable.argtypes = [i32, i64, i32, i32p, i32p, i32p, i32p, P(i32),
                                           ctypes.c_int]
             L.bisim_canonical.argtypes = [i32, P(i64), i32p, ctypes.c_int]
+            L.bisim_is_stable_under.argtypes = [i32, i64, i32, i32p, i32p, i32p, i32p, i32p, i64,
+                                                P(i32), ctypes.c_int]
             L.bisim_bcrp_sharded.argtypes = [i32, i64, i32, i32p, i32p, i32p, i64, i32p, i32p, i64,
                                              P(Stats), i32p, i32, i32]
             L.bisim_rcpp_sharded.argtypes = [i32, i64, i32p, i32p, i32p, i64, i32p, i32p, i64,
@@ -130,7 +132,7 @@ def lib():
                          "bisim_label_partition", "bisim_device_count", "bisim_quotient",
                          "bisim_is_stable", "bisim_canonical", "bisim_aut_parse", "bisim_aut_read_file",
            "bisim_aut_columns", "bisim_aut_label", "bisim_aut_free", "bisim_bcrp_sharded",
-           "bisim_rcpp_sharded"):
+           "bisim_rcpp_sharded", "bisim_is_stable_under"):
                 getattr(L, name).restype = ctypes.c_int
             L.bisim_last_error.restype = ctypes.c_char_p
             L.bisim_last_error.argtypes = []

@@ -165,6 +165,40 @@ __global__ void k_sig_subset(Triples t, int64_t m, unsigned long long seed, cons
     }
 }
 
+// ---- stability under a state set (oracle.py:144-154) -------------------------------
+
+// reach[w * n + s] bit a: s has an a-transition into the set (word-major masks)
+__global__ void k_reach_mask(int32_t n, int64_t m, const int32_t* __restrict__ src, const int32_t* __restrict__ act,
+                             const int32_t* __restrict__ dst, const uint8_t* __restrict__ in_set,
+                             unsigned long long* reach) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        if (!in_set[dst[i]]) continue;
+        const int32_t a = act[i];
+        asm volatile("red.relaxed.gpu.global.or.b64 [%0], %1;" ::"l"(&reach[(int64_t)(a >> 6) * n + src[i]]),
+                     "l"(1ull << (a & 63))
+                     : "memory");
+    }
+}
+
+__global__ void k_reach_check(int32_t n, int32_t W, const int32_t* __restrict__ block,
+                              const unsigned long long* __restrict__ reach, int32_t* unstable) {
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t l = block[s];
+        for (int32_t w = 0; w < W; ++w)
+            if (reach[(int64_t)w * n + s] != reach[(int64_t)w * n + l]) {
+                *unstable = 1;
+                break;
+            }
+    }
+}
+
+__global__ void k_set_flags(int64_t k, const int32_t* __restrict__ states, int32_t n, uint8_t* in_set, int32_t* bad) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t x = states[i];
+        if ((unsigned)x < (unsigned)n) in_set[x] = 1;
+    }
+}
+
 // ---- canonical leader form (lts.py:117-128) --------------------------------------
 
 __device__ __forceinline__ unsigned long long value_hash(long long v, unsigned long long seed) {
@@ -394,6 +428,57 @@ int bisim_is_stable(int32_t n, int64_t m, int32_t num_actions, const int32_t* sr
                                                                unstable);
         }
         k_sig_check<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, d_block, cnt, unstable);
+        CK(cudaGetLastError());
+        *stable_out = read_flag(c, unstable) ? 0 : 1;
+        return BISIM_OK;
+    });
+}
+
+int bisim_is_stable_under(int32_t n, int64_t m, int32_t num_actions, const int32_t* src, const int32_t* act,
+                          const int32_t* dst, const int32_t* block, const int32_t* states, int64_t num_states,
+                          int32_t* stable_out, int device) {
+    using namespace bisim;
+    return post_guarded([&]() -> int {
+        if (n < 1) throw Error(BISIM_BAD_INPUT, "state count must be at least 1");
+        if (m < 0 || m >= (int64_t)INT32_MAX) throw Error(BISIM_BAD_INPUT, "transition count out of range");
+        if (num_states < 0) throw Error(BISIM_BAD_INPUT, "negative state-set size");
+        if (!block || !stable_out || (m && (!src || !act || !dst)) || (num_states && !states))
+            throw Error(BISIM_BAD_INPUT, "null array");
+        Ctx& c = *get_ctx(device);
+        std::lock_guard<std::mutex> lock(c.mu);
+        post_begin(c);
+        cudaStream_t st = c.stream;
+        const int TB = 256;
+        const int64_t mm = std::max<int64_t>(m, 1);
+        const int32_t W = std::max(1, (num_actions + 63) / 64);
+        int32_t* d_src = (int32_t*)c.src.ensure(mm * 4);
+        int32_t* d_act = (int32_t*)c.act.ensure(mm * 4);
+        int32_t* d_dst = (int32_t*)c.dst.ensure(mm * 4);
+        int32_t* d_block = (int32_t*)c.block.ensure((int64_t)n * 4);
+        int32_t* d_states = (int32_t*)c.pi0.ensure(std::max<int64_t>(num_states, 1) * 4);
+        if (m) {
+            CK(cudaMemcpyAsync(d_src, src, m * 4, cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(d_act, act, m * 4, cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(d_dst, dst, m * 4, cudaMemcpyHostToDevice, st));
+        }
+        CK(cudaMemcpyAsync(d_block, block, (int64_t)n * 4, cudaMemcpyHostToDevice, st));
+        if (num_states) CK(cudaMemcpyAsync(d_states, states, num_states * 4, cudaMemcpyHostToDevice, st));
+        check_transitions(c, n, m, num_actions, d_src, d_act, d_dst);
+        int32_t* bad = (int32_t*)c.counter.ensure(16);
+        int32_t* flags = (int32_t*)c.bstart.ensure(((int64_t)n + 1) * 4);
+        CK(cudaMemsetAsync(flags, 0, ((int64_t)n + 1) * 4, st));
+        CK(cudaMemsetAsync(bad, 0, 8, st));
+        k_leader_flags<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, d_block, flags, bad);
+        CK(cudaGetLastError());
+        if (read_flag(c, bad)) throw Error(BISIM_BAD_INPUT, "block array is not a leader-form partition");
+        uint8_t* in_set = (uint8_t*)c.scnt.ensure((int64_t)n);
+        CK(cudaMemsetAsync(in_set, 0, (int64_t)n, st));
+        if (num_states) k_set_flags<<<grid_for(num_states, TB, c.sms), TB, 0, st>>>(num_states, d_states, n, in_set, bad);
+        auto* reach = (unsigned long long*)c.lmask.ensure((size_t)W * n * 8);
+        CK(cudaMemsetAsync(reach, 0, (size_t)W * n * 8, st));
+        if (m) k_reach_mask<<<grid_for(m, TB, c.sms), TB, 0, st>>>(n, m, d_src, d_act, d_dst, in_set, reach);
+        int32_t* unstable = bad + 1;
+        k_reach_check<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, W, d_block, reach, unstable);
         CK(cudaGetLastError());
         *stable_out = read_flag(c, unstable) ? 0 : 1;
         return BISIM_OK;

@@ -5,7 +5,8 @@
   blocks numbered densely in leader order, duplicate transitions merged in
   first-occurrence order.
 * :func:`is_stable` -- every state sees the same (action, target block) pairs
-  as its leader (/root/reference/pkg/src/parbisim/oracle.py:128-141).
+  as its leader (/root/reference/pkg/src/parbisim/oracle.py:128-141);
+  :func:`is_stable_under` -- the same for one target set (oracle.py:144-154).
 * :func:`canonical_arrays` -- leader form of an arbitrary id assignment
   (/root/reference/pkg/src/parbisim/lts.py:117-128), for assignments too
   large for host code.
@@ -83,6 +84,30 @@ def is_stable(lts, partition, device: int = 0) -> bool:
     return is_stable_arrays(n, src, act, dst, A, np.asarray(partition.block, np.int32), device)
 
 
+def is_stable_under_arrays(n: int, src, act, dst, num_actions: int, block, states,
+                           device: int = 0) -> bool:
+    src, act, dst, block = (N.as_i32(x) for x in (src, act, dst, block))
+    if block.size != n:
+        raise ValueError("partition covers a different number of states")
+    st = np.ascontiguousarray(np.fromiter((int(x) for x in states), dtype=np.int64))
+    st = st[(st >= 0) & (st < n)].astype(np.int32)  # other ids are never reached
+    out = ctypes.c_int32(0)
+    _check(N.lib().bisim_is_stable_under(n, src.size, int(num_actions), N.ptr(src), N.ptr(act),
+                                         N.ptr(dst), N.ptr(block), N.ptr(st), st.size,
+                                         ctypes.byref(out), device))
+    return bool(out.value)
+
+
+def is_stable_under(lts, partition, states, device: int = 0) -> bool:
+    """True when every block either wholly reaches ``states`` via each action
+    or wholly avoids it (oracle.py:144-154)."""
+    if len(partition) != lts.n:
+        raise ValueError("partition covers a different number of states")
+    n, src, act, dst, A = lts_columns(lts)
+    return is_stable_under_arrays(n, src, act, dst, A, np.asarray(partition.block, np.int32),
+                                  states, device)
+
+
 def canonical_arrays(assignment, device: int = 0) -> np.ndarray:
     """Leader form of an id assignment: states sharing an id share a block led
     by its smallest state (lts.py:117-128).  Ids are int64."""
@@ -99,5 +124,5 @@ def canonical_partition(assignment, device: int = 0) -> Partition:
     return Partition(canonical_arrays(assignment, device), _trusted=True)
 
 
-__all__ = ["quotient", "quotient_arrays", "is_stable", "is_stable_arrays", "canonical_arrays",
-           "canonical_partition"]
+__all__ = ["quotient", "quotient_arrays", "is_stable", "is_stable_arrays", "is_stable_under",
+           "is_stable_under_arrays", "canonical_arrays", "canonical_partition"]

@@ -59,6 +59,17 @@ def test_oracle_is_stable_matches_reference_fixtures():
             assert PO.is_stable(n, src, act, dst, p["block"]) == p["stable"], name
 
 
+def test_oracle_is_stable_under_matches_reference_fixtures():
+    verdicts = []
+    for rec in post_cases():
+        n, src, act, dst, _ = _arrays(rec)
+        for name, p in rec["partitions"].items():
+            for sub, exp in p["under"]:
+                assert PO.is_stable_under(n, src, act, dst, p["block"], sub) == exp, name
+                verdicts.append(exp)
+    assert any(verdicts) and not all(verdicts)
+
+
 def test_oracle_canonical_matches_reference_fixtures():
     for rec in post_cases():
         assert PO.canonical(rec["assignment"]).tolist() == rec["canonical"]
@@ -102,6 +113,16 @@ def test_gpu_is_stable_matches_reference_fixtures():
         n, src, act, dst, A = _arrays(rec)
         for name, p in rec["partitions"].items():
             assert is_stable_arrays(n, src, act, dst, A, p["block"]) == p["stable"], name
+
+
+@pytest.mark.gpu
+def test_gpu_is_stable_under_matches_reference_fixtures():
+    from paper_2105_11788_b200.post import is_stable_under_arrays
+    for rec in post_cases():
+        n, src, act, dst, A = _arrays(rec)
+        for name, p in rec["partitions"].items():
+            for sub, exp in p["under"]:
+                assert is_stable_under_arrays(n, src, act, dst, A, p["block"], sub) == exp, name
 
 
 @pytest.mark.gpu
@@ -160,6 +181,16 @@ def test_gpu_post_vs_oracle_medium(seed):
         assert np.array_equal(x, y)
     assert is_stable_arrays(n, src, act, dst, A, block) == PO.is_stable(n, src, act, dst, block)
     assert is_stable_arrays(n, src, act, dst, A, np.arange(n)) is True
+    from paper_2105_11788_b200.post import is_stable_under_arrays
+    for sub in (np.nonzero(block == block[5])[0], g.choice(n, 5000, replace=False), [n + 3, -1]):
+        assert (is_stable_under_arrays(n, src, act, dst, A, block, sub)
+                == PO.is_stable_under(n, src, act, dst, block, sub))
+    # a 70-label system: two mask words per state
+    act70 = g.integers(0, 70, m).astype(np.int32)
+    sub = g.choice(n, 3000, replace=False)
+    for blk in (block, np.arange(n)):
+        assert (is_stable_under_arrays(n, src, act70, dst, 70, blk, sub)
+                == PO.is_stable_under(n, src, act70, dst, blk, sub))
 
 
 @pytest.mark.gpu
