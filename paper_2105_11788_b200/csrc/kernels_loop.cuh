@@ -408,9 +408,15 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
         } else {
             // one pass: every work item has its own warp; all warps of the
             // CTA take part (the big-chunk path synchronises the CTA)
+            // blocks of a few chunks each: items go to warps in CTA-major
+            // order, so a block's chunks share a CTA and combine in shared
+            // memory without a global arrival (c4l -7 %); larger blocks keep
+            // the CTA-minor spread (c5: CTA-major 1.5 % slower)
+            const bool major = !solo && p.onepass_major && nch <= (kSparseThreads / 32) * max(nbig, 1);
+            const int32_t twb = major ? (int32_t)(gtid >> 5) : tw;
             int32_t cnt = 0;
-            if (tw < nsm) cnt = process_small<IDENT>(p, cur, round, C, p.small_list[tw]);
-            const int32_t ci = tw >= nsm && tw < nsm + nch ? tw - nsm : -1;
+            if (twb < nsm) cnt = process_small<IDENT>(p, cur, round, C, p.small_list[twb]);
+            const int32_t ci = twb >= nsm && twb < nsm + nch ? twb - nsm : -1;
             if (mode_b == 0) cnt += big_onepass_cta<IDENT, 1>(p, cur, round, C, nbig, ci, s_slot);
             else cnt += big_onepass_cta<IDENT, kWide>(p, cur, round, C, nbig, ci, s_slot);
             if (lane == 0) my_members += (unsigned long long)cnt;
