@@ -388,7 +388,9 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
             if (SH) p.peer_xcnt[p.shard][nxt] = 0;
         }
         // chunk layout and pass count for this round (kernels_big.cuh)
-        int mode_b = nsm + nch1 <= tnw ? 0 : (nsm + nch4 <= tnw ? 1 : 2);
+        // one pass needs a warp per big-block chunk only: small blocks are
+        // independent items that any warp takes on the side
+        int mode_b = nch1 <= tnw ? 0 : (nch4 <= tnw ? 1 : 2);
         // a few very large blocks (> 16K members each on average): the wide
         // layout keeps a quarter of the warps busy with 4 loads in flight per
         // lane, which measured faster than every warp holding one chunk
@@ -415,8 +417,11 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
             const bool major = !solo && p.onepass_major && nch <= (kSparseThreads / 32) * max(nbig, 1);
             const int32_t twb = major ? (int32_t)(gtid >> 5) : tw;
             int32_t cnt = 0;
-            if (twb < nsm) cnt = process_small<IDENT>(p, cur, round, C, p.small_list[twb]);
-            const int32_t ci = twb >= nsm && twb < nsm + nch ? twb - nsm : -1;
+            // small blocks first go to the warps without a chunk (ids nch..)
+            int32_t it = twb - nch;
+            if (it < 0) it += tnw;
+            for (; it < nsm; it += tnw) cnt += process_small<IDENT>(p, cur, round, C, p.small_list[it]);
+            const int32_t ci = twb < nch ? twb : -1;
             if (mode_b == 0) cnt += big_onepass_cta<IDENT, 1>(p, cur, round, C, nbig, ci, s_slot);
             else cnt += big_onepass_cta<IDENT, kWide>(p, cur, round, C, nbig, ci, s_slot);
             if (lane == 0) my_members += (unsigned long long)cnt;
