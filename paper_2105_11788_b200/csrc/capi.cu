@@ -502,7 +502,6 @@ int run_with(Ctx& c, Job& j) {
         sp.allow_solo = getenv("BISIM_NO_SOLO") == nullptr ? 1 : 0;
         // developer: BISIM_MODE_B=1|2 forces the wide / two-pass phase-B layout
         sp.force_mode_b = getenv("BISIM_MODE_B") ? atoi(getenv("BISIM_MODE_B")) : -1;
-        sp.pad_exp = getenv("BISIM_EXP") ? atoi(getenv("BISIM_EXP")) : 0;
         sp.batch_min_c = getenv("BISIM_BATCH_C") ? atoi(getenv("BISIM_BATCH_C")) : 8192;
         sp.onepass_major = getenv("BISIM_ONEPASS_MINOR") == nullptr ? 1 : 0;
         sp.solo_max_c = getenv("BISIM_SOLO_C") ? atoi(getenv("BISIM_SOLO_C")) : kSoloMaxC;

@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
                         // reverse edges stream through (evict-first), so they do not push
                         // the randomly accessed per-state arrays out of L2
                         if (IDENT) rv[u] = make_int2(0, act[u] ? __ldcs(&p.rev_src[s[u]]) : 0);
-                        else rv[u] = act[u] ? (p.pad_exp == 2 ? p.rev[s[u]] : __ldcs(&p.rev[s[u]])) : make_int2(0, 0);
+                        else rv[u] = act[u] ? __ldcs(&p.rev[s[u]]) : make_int2(0, 0);
                     }
 #pragma unroll
                     for (int u = 0; u < kA; ++u) {

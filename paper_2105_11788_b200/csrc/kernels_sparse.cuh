@@ -184,7 +184,6 @@ struct SparseParams {
     int32_t force_mode_b;       // developer override of the phase-B layout (-1: automatic)
     int32_t solo_max_c;         // solo stretches: splitter size and previous-round work
     int32_t solo_max_items;     //   item limits (kernels_loop.cuh)
-    int32_t pad_exp;            // developer experiment switch (BISIM_EXP)
     int32_t batch_min_c;        // splitter size from which phase A registers blocks in one wave
     int32_t onepass_major;      // one-pass phase B: CTA-major item placement
     // ---- transition-sharded mode (kernels_shard.cuh); nshard == 1 otherwise
