@@ -19,7 +19,7 @@
 // measured on c1 / c2 (512-thread CTAs): 16 / 128 beat 64 / 64 by 6 / 3 %
 constexpr int32_t kSoloMaxC = 16;
 constexpr int32_t kSoloMaxItems = 128;
-constexpr int32_t kSoloSkipSpan = 1024;  // skip-step window of the solo team
+constexpr int32_t kSoloSkipSpan = 512;   // skip-step window of the solo team: one label per thread
 #ifndef BISIM_KA
 #define BISIM_KA 2
 #endif
