@@ -27,6 +27,9 @@
 // label tables are merged and sorted once, then local ids are remapped.
 #include <algorithm>
 #include <cstdint>
+#include <new>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <string_view>
@@ -45,12 +48,47 @@ namespace bisim {
 void set_last_error(const std::string& msg);
 }
 
+namespace {
+
+// An int32 column of up to `cap` entries in anonymous memory advised for
+// transparent huge pages: filling hundreds of MB of 4 KB pages from several
+// threads is page-fault bound.  Pages are touched by the writing thread.
+struct Column {
+    int32_t* p = nullptr;
+    size_t cap = 0, n = 0;
+    size_t bytes = 0;
+    void alloc(size_t c) {
+        cap = c;
+        bytes = std::max<size_t>(c * 4, 4096);
+        void* m = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+        if (m == MAP_FAILED) throw std::bad_alloc();
+        madvise(m, bytes, MADV_HUGEPAGE);
+        p = (int32_t*)m;
+    }
+    void push(int32_t v) { p[n++] = v; }
+    Column() = default;
+    Column(const Column&) = delete;
+    Column& operator=(const Column&) = delete;
+    Column(Column&& o) noexcept : p(o.p), cap(o.cap), n(o.n), bytes(o.bytes) { o.p = nullptr; }
+    ~Column() {
+        if (p) munmap(p, bytes);
+    }
+};
+
+// Parsed columns of one chunk: (source, local label id, target).
+struct Parsed {
+    Column src, lab, dst;
+    std::vector<int32_t> rank;  // local label id -> action id
+};
+
+}  // namespace
+
 struct bisim_aut {
     int32_t n = 0;
     int32_t initial = 0;
     int64_t m = 0;
     std::vector<std::string> labels;
-    std::vector<int32_t> src, act, dst;
+    std::vector<Parsed> parts;  // in file order; action ids via each part's rank
 };
 
 namespace {
@@ -232,13 +270,16 @@ bool match_header(string_view line, string (&num)[3]) {
 
 // ---- one transition line (aut.py:48-76) -----------------------------------
 
-struct Chunk {
+// Each chunk is written by one thread only: cache-line aligned so that the
+// vectors' bookkeeping of neighbouring chunks never shares a line (false
+// sharing on every push_back serialised the threads).
+struct alignas(128) Chunk {
     const char* b = nullptr;
     const char* e = nullptr;
     int64_t lines = 0;          // lines in this chunk
     int64_t fail_line = -1;     // local index of the first failing line
     string fail_msg;
-    std::vector<int32_t> src, lab, dst;
+    Parsed out;
     std::vector<string_view> labels;  // local id -> label text
 };
 
@@ -306,6 +347,11 @@ string parse_transition(string_view line, int32_t n, int32_t& s_out, string_view
 }
 
 void parse_chunk(Chunk& c, int32_t n, bool skip_first_line) {
+    // one allocation per column (a transition line is at least 7 bytes)
+    const size_t cap = (size_t)(c.e - c.b) / 7 + 16;
+    c.out.src.alloc(cap);
+    c.out.lab.alloc(cap);
+    c.out.dst.alloc(cap);
     std::unordered_map<string_view, int32_t, SvHash> ids;
     string_view last_label;
     int32_t last_id = -1;
@@ -344,9 +390,9 @@ void parse_chunk(Chunk& c, int32_t n, bool skip_first_line) {
             last_label = label;
             last_id = id;
         }
-        c.src.push_back(s);
-        c.lab.push_back(id);
-        c.dst.push_back(t);
+        c.out.src.push(s);
+        c.out.lab.push(id);
+        c.out.dst.push(t);
     }
     c.lines = li;
 }
@@ -403,6 +449,7 @@ bisim_aut* parse(const char* text, int64_t len, int32_t threads, ParseFail& fail
         parse_chunk(ch[0], n, true);
         for (auto& t : pool) t.join();
     }
+
     int64_t line0 = 0, count = 0;
     for (auto& c : ch) {
         if (c.fail_line >= 0) {
@@ -410,7 +457,7 @@ bisim_aut* parse(const char* text, int64_t len, int32_t threads, ParseFail& fail
             return nullptr;
         }
         line0 += c.lines;
-        count += (int64_t)c.src.size();
+        count += (int64_t)c.out.src.n;
     }
     if (!mm.fits || count != mm.value) {
         fail = {0, "expected " + mm.text + " transitions, found " + std::to_string(count)};
@@ -427,26 +474,11 @@ bisim_aut* parse(const char* text, int64_t len, int32_t threads, ParseFail& fail
     a->m = count;
     a->labels.reserve(all.size());
     for (auto v : all) a->labels.emplace_back(v);
-    a->src.resize((size_t)count);
-    a->act.resize((size_t)count);
-    a->dst.resize((size_t)count);
-    std::vector<int64_t> base(T, 0);
-    for (int k = 1; k < T; ++k) base[k] = base[k - 1] + (int64_t)ch[k - 1].src.size();
-    auto fill = [&](int k) {
-        Chunk& c = ch[k];
-        std::vector<int32_t> rank(c.labels.size());
+    for (auto& c : ch) {
+        c.out.rank.resize(c.labels.size());
         for (size_t i = 0; i < c.labels.size(); ++i)
-            rank[i] = (int32_t)(std::lower_bound(all.begin(), all.end(), c.labels[i]) - all.begin());
-        const size_t o = (size_t)base[k];
-        std::copy(c.src.begin(), c.src.end(), a->src.begin() + o);
-        std::copy(c.dst.begin(), c.dst.end(), a->dst.begin() + o);
-        for (size_t i = 0; i < c.lab.size(); ++i) a->act[o + i] = rank[c.lab[i]];
-    };
-    {
-        std::vector<std::thread> pool;
-        for (int k = 1; k < T; ++k) pool.emplace_back(fill, k);
-        fill(0);
-        for (auto& t : pool) t.join();
+            c.out.rank[i] = (int32_t)(std::lower_bound(all.begin(), all.end(), c.labels[i]) - all.begin());
+        a->parts.push_back(std::move(c.out));
     }
     return a;
 }
@@ -522,9 +554,20 @@ int bisim_aut_read_file(const char* path, int32_t threads, bisim_aut** out, bisi
 
 int bisim_aut_columns(const bisim_aut* a, int32_t* src, int32_t* act, int32_t* dst) {
     if (!a) return BISIM_BAD_INPUT;
-    std::copy(a->src.begin(), a->src.end(), src);
-    std::copy(a->act.begin(), a->act.end(), act);
-    std::copy(a->dst.begin(), a->dst.end(), dst);
+    // one thread per parsed chunk: copy sources and targets, remap labels
+    std::vector<size_t> base(a->parts.size() + 1, 0);
+    for (size_t k = 0; k < a->parts.size(); ++k) base[k + 1] = base[k] + a->parts[k].src.n;
+    auto fill = [&](size_t k) {
+        const Parsed& q = a->parts[k];
+        const size_t o = base[k];
+        std::memcpy(src + o, q.src.p, q.src.n * 4);
+        std::memcpy(dst + o, q.dst.p, q.dst.n * 4);
+        for (size_t i = 0; i < q.lab.n; ++i) act[o + i] = q.rank[q.lab.p[i]];
+    };
+    std::vector<std::thread> pool;
+    for (size_t k = 1; k < a->parts.size(); ++k) pool.emplace_back(fill, k);
+    if (!a->parts.empty()) fill(0);
+    for (auto& t : pool) t.join();
     return BISIM_OK;
 }
 
