@@ -529,22 +529,40 @@ int bisim_aut_read_file(const char* path, int32_t threads, bisim_aut** out, bisi
         struct stat sb;
         fstat(fd, &sb);
         const int64_t len = sb.st_size;
-        const char* text = nullptr;
-        void* map = nullptr;
+        // read into a huge-page buffer with one pread per thread (a file
+        // mapping would fault in 4 KB pages one by one)
+        Column buf;
         if (len > 0) {
-            map = mmap(nullptr, (size_t)len, PROT_READ, MAP_PRIVATE, fd, 0);
-            if (map == MAP_FAILED) {
-                close(fd);
-                bisim::set_last_error(string("cannot map ") + path);
-                return BISIM_BAD_INPUT;
-            }
-            madvise(map, (size_t)len, MADV_SEQUENTIAL);
-            text = (const char*)map;
+            buf.alloc((size_t)(len + 3) / 4);
+            int T = threads > 0 ? threads : (int)std::max(1u, std::thread::hardware_concurrency());
+            T = (int)std::min<int64_t>(T, std::max<int64_t>(1, len / (8 << 20)));
+            std::vector<int> ok(T, 1);
+            auto rd = [&](int k) {
+                int64_t lo = len * k / T, hi = len * (k + 1) / T;
+                char* d = (char*)buf.p;
+                while (lo < hi) {
+                    const ssize_t r = pread(fd, d + lo, (size_t)(hi - lo), lo);
+                    if (r <= 0) {
+                        ok[k] = 0;
+                        return;
+                    }
+                    lo += r;
+                }
+            };
+            std::vector<std::thread> pool;
+            for (int k = 1; k < T; ++k) pool.emplace_back(rd, k);
+            rd(0);
+            for (auto& t : pool) t.join();
+            for (int v : ok)
+                if (!v) {
+                    close(fd);
+                    bisim::set_last_error(string("cannot read ") + path);
+                    return BISIM_BAD_INPUT;
+                }
         }
-        ParseFail f;
-        bisim_aut* a = parse(text, len, threads, f);
-        if (map) munmap(map, (size_t)len);
         close(fd);
+        ParseFail f;
+        bisim_aut* a = parse((const char*)buf.p, len, threads, f);
         return finish(a, f, out, info);
     } catch (const std::exception& e) {
         bisim::set_last_error(e.what());
