@@ -1165,7 +1165,7 @@ void* bisim_stream(int device) {
     }
 }
 
-const char* bisim_version(void) { return "libbisim 0.1 (sm_100a, dense persistent loop)"; }
+const char* bisim_version(void) { return "libbisim 0.2 (sm_100a: work-efficient persistent refinement loop, sharded replicas, GPU quotient/stability, C++ .aut reader)"; }
 
 }  // extern "C"
 
