@@ -504,6 +504,7 @@ int run_with(Ctx& c, Job& j) {
         sp.force_mode_b = getenv("BISIM_MODE_B") ? atoi(getenv("BISIM_MODE_B")) : -1;
         sp.batch_min_c = getenv("BISIM_BATCH_C") ? atoi(getenv("BISIM_BATCH_C")) : 8192;
         sp.onepass_major = getenv("BISIM_ONEPASS_MINOR") == nullptr ? 1 : 0;
+        sp.prefetch_next = getenv("BISIM_PREFETCH") ? atoi(getenv("BISIM_PREFETCH")) : 1;
         sp.solo_max_c = getenv("BISIM_SOLO_C") ? atoi(getenv("BISIM_SOLO_C")) : kSoloMaxC;
         sp.solo_max_items = getenv("BISIM_SOLO_ITEMS") ? atoi(getenv("BISIM_SOLO_ITEMS")) : kSoloMaxItems;
         // developer tracing: BISIM_TRACE=<rounds> BISIM_TRACE_FILE=<path>

@@ -224,12 +224,24 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
         // ---- phase A: mark the in-edges of C's members ----------------------
         if (aux) {
             const int32_t sc = u_clear_next_warp(p, C);
+            int2 sr = make_int2(0, 0);
             if (lane == 0) {
                 ctl->succ[cur] = sc;
                 ctl->next_min[cur] = kBig;
                 // the usual next splitter: fetch its member range now (it
                 // cannot change this round unless the label is raised again)
-                if (sc != kBig) ctl->succ_range[cur] = p.brange[sc];
+                if (sc != kBig) {
+                    sr = p.brange[sc];
+                    ctl->succ_range[cur] = sr;
+                }
+            }
+            if (p.prefetch_next) {
+                // and pull its member records towards L2 for the next phase A
+                sr.x = __shfl_sync(kFull, sr.x, 0);
+                sr.y = __shfl_sync(kFull, sr.y, 0);
+                const int32_t lines = min((sr.y + 7) >> 3, 1024);
+                for (int32_t k = lane; k < lines; k += 32)
+                    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p.members + sr.x + 8 * k));
             }
         }
         {

@@ -186,6 +186,7 @@ struct SparseParams {
     int32_t solo_max_items;     //   item limits (kernels_loop.cuh)
     int32_t batch_min_c;        // splitter size from which phase A registers blocks in one wave
     int32_t onepass_major;      // one-pass phase B: CTA-major item placement
+    int32_t prefetch_next;      // phase A: prefetch the likely next splitter's member records
     // ---- transition-sharded mode (kernels_shard.cuh); nshard == 1 otherwise
     int32_t nshard;                       // replicas taking part in every round
     int32_t shard;                        // my index
