@@ -129,8 +129,8 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
                 __syncthreads();
                 fresh = false;
             }
-            const bool stay = p.brange[C].y <= p.solo_max_c &&
-                              ld_vol(&ctl->items_last) <= p.solo_max_items;
+            const int32_t csz = cr_c == C ? cr_v.y : p.brange[C].y;
+            const bool stay = csz <= p.solo_max_c && s_items_last <= p.solo_max_items;
             if (!stay) {
                 if (threadIdx.x == 0) {
                     ctl->C0 = C;
@@ -233,6 +233,10 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
                 if (sc != kBig) {
                     sr = p.brange[sc];
                     ctl->succ_range[cur] = sr;
+                }
+                if (solo) {
+                    s_succ = sc;
+                    s_succ_range = sr;
                 }
             }
             if (p.prefetch_next) {
@@ -339,7 +343,7 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
                             }
                         }
                         if (__any_sync(kFull, reg)) {
-                            register_blocks_warp(p, cur, reg, b[u]);
+                            register_blocks_warp(p, cur, reg, b[u], solo);
                             if (SH && reg) shard_publish(p, cur, b[u]);
                         }
                     }
@@ -359,7 +363,7 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
                         reg = !(atomicOr(&p.tblock[b >> 5], bit) & bit);
                     }
                     if (__any_sync(kFull, reg)) {
-                        register_blocks_warp(p, cur, reg, b);
+                        register_blocks_warp(p, cur, reg, b, solo);
                         if (SH && reg) shard_publish(p, cur, b);
                     }
                 }
@@ -373,9 +377,17 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
             shard_merge(p, cur, tw, tnw, s_snap);
         }
         team_barrier(solo, p.bar, gen, [&] {
-            s_snap[0] = ld_vol(&ctl->n_small[cur]);
-            s_snap[1] = (long long)ld_vol(&ctl->big_pack[cur]);
-            s_snap[2] = (long long)ld_vol(&ctl->big_pack4[cur]);
+            if (solo) {
+                s_snap[0] = s_ctr_nsmall;
+                s_snap[1] = (long long)s_ctr_big;
+                s_snap[2] = (long long)s_ctr_big4;
+                s_ctr_nsmall = 0;  // the phase-A counters of the next solo round
+                s_ctr_big = s_ctr_big4 = 0ull;
+            } else {
+                s_snap[0] = ld_vol(&ctl->n_small[cur]);
+                s_snap[1] = (long long)ld_vol(&ctl->big_pack[cur]);
+                s_snap[2] = (long long)ld_vol(&ctl->big_pack4[cur]);
+            }
         });
         if (tr) {
             p.trace[round * kTraceWords + 2] = globaltimer();
@@ -397,6 +409,7 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
             ctl->big_pack4[nxt] = 0ull;
             ctl->heavy[nxt] = 0;
             ctl->items_last = nsm + nch1;
+            s_items_last = nsm + nch1;
             if (SH) p.peer_xcnt[p.shard][nxt] = 0;
         }
         // chunk layout and pass count for this round (kernels_big.cuh)
@@ -440,13 +453,26 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
         }
         for (int k = threadIdx.x; k < kSeen; k += blockDim.x) s_seen[k] = -1;
         team_barrier(solo, p.bar, gen, [&] { raise_flush_warp0(p, cur, round); }, [&] {
-            const int32_t nm = ld_vol(&ctl->next_min[cur]), sc = ld_vol(&ctl->succ[cur]);
-            const int32_t* sr = (const int32_t*)&ctl->succ_range[cur];
-            const int32_t sx = ld_vol(sr), sy = ld_vol(sr + 1);
+            int32_t nm, sc, sx, sy;
+            if (solo) {  // everything this round raised or found is in this CTA
+                nm = s_nmin_round;
+                sc = s_succ;
+                sx = s_succ_range.x;
+                sy = s_succ_range.y;
+                s_snap[4] = s_ctr_heavy;
+                s_ctr_heavy = 0;
+                s_snap[5] = s_items_last;
+            } else {
+                nm = ld_vol(&ctl->next_min[cur]);
+                sc = ld_vol(&ctl->succ[cur]);
+                const int32_t* sr = (const int32_t*)&ctl->succ_range[cur];
+                sx = ld_vol(sr);
+                sy = ld_vol(sr + 1);
+                s_snap[4] = ld_vol(&ctl->heavy[cur]);
+                s_snap[5] = ld_vol(&ctl->items_last);
+            }
             const int32_t c_next = min(nm, sc);
             s_snap[3] = c_next;
-            s_snap[4] = ld_vol(&ctl->heavy[cur]);
-            s_snap[5] = ld_vol(&ctl->items_last);
             if (c_next != kBig) {
                 if (nm > sc) {
                     s_snap[6] = ((long long)sy << 32) | (unsigned)sx;

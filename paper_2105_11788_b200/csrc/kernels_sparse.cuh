@@ -231,6 +231,18 @@ __shared__ int32_t s_ndirty;
 __shared__ uint32_t s_u2[32];
 __shared__ int32_t s_nmin;
 __shared__ int32_t s_nsplit;
+__shared__ int32_t s_nmin_round;  // raised minimum of the phase just flushed
+
+// Round control of a solo stretch (CTA 0 alone): the registration counters,
+// the successor and its range, the previous round's item count live in
+// shared memory, so a solo round's phases hand over without global round
+// trips (kernels_loop.cuh).
+__shared__ int32_t s_ctr_nsmall;
+__shared__ unsigned long long s_ctr_big, s_ctr_big4;
+__shared__ int32_t s_ctr_heavy;
+__shared__ int32_t s_succ;
+__shared__ int2 s_succ_range;
+__shared__ int32_t s_items_last;
 
 __device__ __forceinline__ void raise_init() {
     for (int k = threadIdx.x; k < kU1Smem; k += blockDim.x) s_u1[k] = 0u;
@@ -239,6 +251,13 @@ __device__ __forceinline__ void raise_init() {
         s_nmin = 0x7fffffff;
         s_nsplit = 0;
         s_ndirty = 0;
+        s_nmin_round = 0x7fffffff;
+        s_ctr_nsmall = 0;
+        s_ctr_big = s_ctr_big4 = 0ull;
+        s_ctr_heavy = 0;
+        s_succ = 0x7fffffff;
+        s_succ_range = make_int2(0, 0);
+        s_items_last = 0x7fffffff;
     }
 }
 
@@ -260,6 +279,7 @@ __device__ __forceinline__ void u_set(const SparseParams& p, int32_t x) {
 __device__ __forceinline__ void raise_flush_warp0(const SparseParams& p, int cur, int64_t round) {
     const int lane = threadIdx.x & 31;
     const int32_t ns = s_nsplit;
+    if (lane == 0) s_nmin_round = ns ? s_nmin : 0x7fffffff;
     if (!ns) return;
     const int32_t nd = s_ndirty;
     for (int k = lane; k < nd; k += 32) {
@@ -374,8 +394,12 @@ __device__ int32_t u_next_warp(const SparseParams& p, int32_t from) {
 // lanes of a warp register at once (warp-uniform call): one counter atomic
 // and one `heavy` store per warp instead of one per block -- thousands of
 // blocks are registered per round in the big rounds of c2/c1.
-__device__ __forceinline__ void register_blocks_warp(const SparseParams& p, int cur, bool reg, int32_t b) {
+__device__ __forceinline__ void register_blocks_warp(const SparseParams& p, int cur, bool reg, int32_t b,
+                                                     bool solo = false) {
     SCtrl* ctl = p.ctrl;
+    // counters: the CTA's shared copies in a solo round, else the global
+    // ones (separate code per address space: a generic-pointer atomic costs
+    // the grid rounds a few percent)
     const int lane = threadIdx.x & 31;
     int2 r = make_int2(0, 0);
     int32_t ob = 0, nb = 0;
@@ -385,12 +409,15 @@ __device__ __forceinline__ void register_blocks_warp(const SparseParams& p, int 
         nb = p.off ? p.off[b + 1] - ob : 1;
     }
     const unsigned heavy = __ballot_sync(kFull, reg && r.y > 1);
-    if (heavy && lane == __ffs(heavy) - 1) ctl->heavy[cur] = 1;
+    if (heavy && lane == __ffs(heavy) - 1) {
+        if (solo) s_ctr_heavy = 1;
+        else ctl->heavy[cur] = 1;
+    }
     const unsigned small = __ballot_sync(kFull, reg && r.y <= 32);
     if (small) {
         const int ld = __ffs(small) - 1;
         int32_t base = 0;
-        if (lane == ld) base = atomicAdd(&ctl->n_small[cur], __popc(small));
+        if (lane == ld) base = solo ? atomicAdd(&s_ctr_nsmall, __popc(small)) : atomicAdd(&ctl->n_small[cur], __popc(small));
         base = __shfl_sync(kFull, base, ld);
         // (label, start, size | leader slot count << 6, leader slot base)
         if (reg && r.y <= 32)
@@ -398,10 +425,16 @@ __device__ __forceinline__ void register_blocks_warp(const SparseParams& p, int 
     }
     if (reg && r.y > 32) {
         const int32_t nch1 = (r.y + 31) >> 5, nch4 = (r.y + 32 * kWide - 1) / (32 * kWide);
-        const unsigned long long pk =
-            atomicAdd(&ctl->big_pack[cur], (1ull << 32) | (unsigned long long)nch1);
-        const unsigned long long pk4 =
-            atomicAdd(&ctl->big_pack4[cur], (1ull << 32) | (unsigned long long)nch4);
+        const unsigned long long d1 = (1ull << 32) | (unsigned long long)nch1;
+        const unsigned long long d4 = (1ull << 32) | (unsigned long long)nch4;
+        unsigned long long pk, pk4;
+        if (solo) {
+            pk = atomicAdd(&s_ctr_big, d1);
+            pk4 = atomicAdd(&s_ctr_big4, d4);
+        } else {
+            pk = atomicAdd(&ctl->big_pack[cur], d1);
+            pk4 = atomicAdd(&ctl->big_pack4[cur], d4);
+        }
         const int32_t k = (int32_t)(pk >> 32), base = (int32_t)(pk & 0xffffffffu);
         const int32_t k4 = (int32_t)(pk4 >> 32), base4 = (int32_t)(pk4 & 0xffffffffu);
         p.big_list[k] = make_int4(b, r.x, r.y, base);
