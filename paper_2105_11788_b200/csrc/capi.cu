@@ -491,7 +491,7 @@ int run_with(Ctx& c, Job& j) {
         sp.smin = (int32_t*)c.smin.ensure((int64_t)n * 4);
         sp.kcur = (int32_t*)c.kcur.ensure((int64_t)n * 4);
         sp.scur = (int32_t*)c.scur.ensure((int64_t)n * 4);
-        sp.sarr = (int32_t*)c.sarr.ensure((int64_t)n * 4);
+        sp.sarr = (unsigned long long*)c.sarr.ensure((int64_t)n * 8);
         sp.splits = splits;
         sp.ctrl = (SCtrl*)ctrl;
         sp.bar = (GridBarrier*)c.bar.ensure(sizeof(GridBarrier));
@@ -503,7 +503,9 @@ int run_with(Ctx& c, Job& j) {
         // developer: BISIM_MODE_B=1|2 forces the wide / two-pass phase-B layout
         sp.force_mode_b = getenv("BISIM_MODE_B") ? atoi(getenv("BISIM_MODE_B")) : -1;
         sp.batch_min_c = getenv("BISIM_BATCH_C") ? atoi(getenv("BISIM_BATCH_C")) : 8192;
-        sp.onepass_major = getenv("BISIM_ONEPASS_MINOR") == nullptr ? 1 : 0;
+        sp.onepass_major = getenv("BISIM_ONEPASS_MINOR") != nullptr ? 0
+                           : getenv("BISIM_MAJOR") ? atoi(getenv("BISIM_MAJOR")) : kSparseThreads / 32;
+        sp.wide_major = getenv("BISIM_WIDE_MAJOR") ? atoi(getenv("BISIM_WIDE_MAJOR")) : 0;
         sp.prefetch_next = getenv("BISIM_PREFETCH") ? atoi(getenv("BISIM_PREFETCH")) : 1;
         sp.solo_max_c = getenv("BISIM_SOLO_C") ? atoi(getenv("BISIM_SOLO_C")) : kSoloMaxC;
         sp.solo_max_items = getenv("BISIM_SOLO_ITEMS") ? atoi(getenv("BISIM_SOLO_ITEMS")) : kSoloMaxItems;

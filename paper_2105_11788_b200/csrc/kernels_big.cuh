@@ -318,6 +318,19 @@ __device__ void big_split(const SparseParams& p, int cur, int64_t round, int32_t
 // those same-address atomics serialise in L2).  Two __syncthreads: after
 // tagging (counts published), and after the per-CTA cursor reservation.
 
+// Packed arrival word of a big block (one-pass split): arrived chunks |
+// split count | kept count.  One-pass blocks have at most tnw * 32 * kWide
+// members (< 2^21 for any grid of up to 16K warps).
+constexpr int kCntBits = 21;
+constexpr unsigned long long kCntMask = (1ull << kCntBits) - 1ull;
+constexpr int kArrShift = 2 * kCntBits;
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 struct OnePassSlot {
     int32_t key;     // big-list index of the warp's block, -1 if none
     int32_t nsplit;
@@ -325,7 +338,8 @@ struct OnePassSlot {
     int32_t wmin;
     int32_t sbase;   // cursor bases reserved by the CTA leader of the block
     int32_t kbase;
-    int32_t pad[2];
+    int32_t ns;      // the block's split count and new leader, as the CTA leader saw them
+    int32_t w;
 };
 
 // Kept members at bs + kbase + rank (from the head of the range), split
@@ -404,30 +418,45 @@ __device__ int32_t big_onepass_cta(const SparseParams& p, int cur, int64_t round
         nch_b = (bz + 32 * K - 1) / (32 * K);
         if (nch_b > cnt_cta) {  // the block spans CTAs: combine globally
             if (lane == 0) {
+                unsigned long long v = 0ull;
+                bool done = false;
                 if (wid == leader) {
-                    // placement cursors first: kept members fill the range
-                    // from the head, split members from the tail, so the
-                    // bases do not depend on the block's split count and the
-                    // reservation overlaps the arrival wait
-                    const int32_t sb = tot_s ? atomicAdd(&p.scur[l], tot_s) : 0;
-                    const int32_t kbs = tot_k ? atomicAdd(&p.kcur[l], tot_k) : 0;
-                    if (tot_s) {
-                        red_add(&p.scnt[l], tot_s);
-                        red_min(&p.smin[l], mn);
+                    // one acq_rel add on the block's packed word reserves the
+                    // placement bases (kept members fill the range from the
+                    // head, split members from the tail, so the bases do not
+                    // depend on the block's split count), publishes the counts
+                    // and arrives; the released minimum is visible with it
+                    if (tot_s) red_min(&p.smin[l], mn);
+                    const unsigned long long add = ((unsigned long long)cnt_cta << kArrShift) |
+                                                   ((unsigned long long)tot_s << kCntBits) | (unsigned)tot_k;
+                    unsigned long long old;
+                    asm volatile("atom.add.acq_rel.gpu.global.u64 %0, [%1], %2;"
+                                 : "=l"(old) : "l"(&p.sarr[l]), "l"(add) : "memory");
+                    slot[wid].sbase = (int32_t)((old >> kCntBits) & kCntMask);
+                    slot[wid].kbase = (int32_t)(old & kCntMask);
+                    v = old + add;
+                    done = (int32_t)(v >> kArrShift) >= nch_b;  // the last arrival waits for nobody
+                }
+                // only the CTA leader of the block polls the word; the
+                // CTA's other warps of the block read its result after the
+                // CTA barrier below
+#ifdef BISIM_NO_SPIN1
+                if (true) {
+#else
+                if (wid == leader) {
+#endif
+                    while (!done) {
+                        v = ld_acquire_u64(&p.sarr[l]);
+                        done = (int32_t)(v >> kArrShift) >= nch_b;
                     }
-                    // release: count and minimum are visible before the arrival
-                    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(&p.sarr[l]), "r"(cnt_cta)
-                                 : "memory");
-                    slot[wid].sbase = sb;
-                    slot[wid].kbase = kbs;
+                    ns = (int32_t)((v >> kCntBits) & kCntMask);
+                    w = ns ? ld_vol(&p.smin[l]) : kBig;
+                    if (wid == leader) {
+                        slot[wid].ns = ns;
+                        slot[wid].w = w;
+                    }
                 }
-                while (ld_acquire_u32((const unsigned*)&p.sarr[l]) < (unsigned)nch_b) {
-                }
-                ns = ld_vol(&p.scnt[l]);
-                w = ld_vol(&p.smin[l]);
             }
-            ns = __shfl_sync(kFull, ns, 0);
-            w = __shfl_sync(kFull, w, 0);
         } else {
             ns = tot_s;
             w = mn;
@@ -440,6 +469,10 @@ __device__ int32_t big_onepass_cta(const SparseParams& p, int cur, int64_t round
     }
     __syncthreads();
     trace_at(p, round, 11);
+    if (has && nch_b > cnt_cta) {
+        ns = slot[leader].ns;
+        w = slot[leader].w;
+    }
     if (has) {
         if (ns) {
             const int32_t sb = slot[leader].sbase + pre_s, kbs = slot[leader].kbase + pre_k;

@@ -23,6 +23,11 @@ constexpr int32_t kSoloSkipSpan = 512;   // skip-step window of the solo team: o
 #ifndef BISIM_KA
 #define BISIM_KA 2
 #endif
+#ifdef BISIM_NO_CSNAP
+constexpr bool kNoCsnap = true;
+#else
+constexpr bool kNoCsnap = false;
+#endif
 constexpr int kA = BISIM_KA;             // in-edges per lane per phase-A step
 
 template <bool IDENT, bool SH>
@@ -248,8 +253,10 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
                     asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p.members + sr.x + 8 * k));
             }
         }
+        // C's member range this round (also C's range at the end of the
+        // round unless C itself splits)
+        const int2 cr = cr_c == C ? cr_v : p.brange[C];
         {
-            const int2 cr = cr_c == C ? cr_v : p.brange[C];
             const int32_t cs = cr.x, cz = cr.y;
             const bool batch = !solo && cz >= p.batch_min_c;  // CTA-uniform
             // members per warp and iteration: every warp gets the same number
@@ -333,17 +340,26 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
                         const unsigned same = __match_any_sync(kFull, act[u] ? b[u] : -1 - lane);
                         const bool rep = act[u] && lane == __ffs(same) - 1;
                         bool reg = false;
+                        BlockInfo bi{};
                         if (rep) {
                             const int f = cta_first(s_seen, b[u]);
                             if (f == 1 && solo) {
                                 reg = true;  // the solo team is this CTA: its table is exact
+                                bi = block_info(p, b[u]);
                             } else if (f == 2 || (f == 1 && !batch)) {
+                                // the block's info loads overlap the test-and-set
+#ifndef BISIM_NO_PRE
+                                bi = block_info(p, b[u]);
+#endif
                                 const uint32_t bit = 1u << (b[u] & 31);
                                 reg = !(atomicOr(&p.tblock[b[u] >> 5], bit) & bit);
                             }
                         }
                         if (__any_sync(kFull, reg)) {
-                            register_blocks_warp(p, cur, reg, b[u], solo);
+#ifdef BISIM_NO_PRE
+                            if (reg) bi = block_info(p, b[u]);
+#endif
+                            register_blocks_warp(p, cur, reg, b[u], bi, solo);
                             if (SH && reg) shard_publish(p, cur, b[u]);
                         }
                     }
@@ -359,8 +375,12 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
                     const int32_t b = s_seen[k];
                     bool reg = false;
                     if (b >= 0) {
+                        // most source blocks of a huge splitter are met by
+                        // every CTA: a plain load first lets all but the
+                        // early CTAs skip the test-and-set on the hot word
                         const uint32_t bit = 1u << (b & 31);
-                        reg = !(atomicOr(&p.tblock[b >> 5], bit) & bit);
+                        if (!(ld_vol(&p.tblock[b >> 5]) & bit))
+                            reg = !(atomicOr(&p.tblock[b >> 5], bit) & bit);
                     }
                     if (__any_sync(kFull, reg)) {
                         register_blocks_warp(p, cur, reg, b, solo);
@@ -408,6 +428,7 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
             ctl->big_pack[nxt] = 0ull;
             ctl->big_pack4[nxt] = 0ull;
             ctl->heavy[nxt] = 0;
+            ctl->csplit[nxt] = 0;
             ctl->items_last = nsm + nch1;
             s_items_last = nsm + nch1;
             if (SH) p.peer_xcnt[p.shard][nxt] = 0;
@@ -420,6 +441,12 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
         // layout keeps a quarter of the warps busy with 4 loads in flight per
         // lane, which measured faster than every warp holding one chunk
         if (mode_b == 0 && nch1 > 512 * nbig) mode_b = 1;
+        // blocks of a few wide chunks each: the wide layout with CTA-major
+        // placement keeps most blocks inside one CTA, whose chunks combine
+        // in shared memory instead of a global arrival
+        if (mode_b == 0 && p.wide_major > 0 && nch1 > p.onepass_major * nbig && nch4 <= tnw &&
+            nch4 <= p.wide_major * nbig)
+            mode_b = 1;
         if (p.force_mode_b > mode_b) mode_b = p.force_mode_b;
         const int32_t nch = mode_b == 0 ? nch1 : nch4;
         if (tr) p.trace[round * kTraceWords + 13] = mode_b;
@@ -439,7 +466,7 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
             // order, so a block's chunks share a CTA and combine in shared
             // memory without a global arrival (c4l -7 %); larger blocks keep
             // the CTA-minor spread (c5: CTA-major 1.5 % slower)
-            const bool major = !solo && p.onepass_major && nch <= (kSparseThreads / 32) * max(nbig, 1);
+            const bool major = !solo && p.onepass_major > 0 && nch <= p.onepass_major * max(nbig, 1);
             const int32_t twb = major ? (int32_t)(gtid >> 5) : tw;
             int32_t cnt = 0;
             // small blocks first go to the warps without a chunk (ids nch..)
@@ -453,9 +480,10 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
         }
         for (int k = threadIdx.x; k < kSeen; k += blockDim.x) s_seen[k] = -1;
         team_barrier(solo, p.bar, gen, [&] { raise_flush_warp0(p, cur, round); }, [&] {
-            int32_t nm, sc, sx, sy;
+            int32_t nm, sc, sx, sy, cs;
             if (solo) {  // everything this round raised or found is in this CTA
                 nm = s_nmin_round;
+                cs = s_csplit_round;
                 sc = s_succ;
                 sx = s_succ_range.x;
                 sy = s_succ_range.y;
@@ -464,6 +492,7 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
                 s_snap[5] = s_items_last;
             } else {
                 nm = ld_vol(&ctl->next_min[cur]);
+                cs = ld_vol(&ctl->csplit[cur]);
                 sc = ld_vol(&ctl->succ[cur]);
                 const int32_t* sr = (const int32_t*)&ctl->succ_range[cur];
                 sx = ld_vol(sr);
@@ -476,6 +505,10 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
             if (c_next != kBig) {
                 if (nm > sc) {
                     s_snap[6] = ((long long)sy << 32) | (unsigned)sx;
+                } else if (!kNoCsnap && c_next == C && !cs) {
+                    // C raised again (BCRP re-raise) without splitting: its
+                    // range is unchanged, no dependent load
+                    s_snap[6] = ((long long)cr.y << 32) | (unsigned)cr.x;
                 } else {
                     const int32_t* r = (const int32_t*)&p.brange[c_next];
                     s_snap[6] = ((long long)ld_vol(r + 1) << 32) | (unsigned)ld_vol(r);

@@ -111,6 +111,7 @@ struct SCtrl {
     unsigned long long work_edges;      // sum of in(C)
     unsigned long long work_members;    // sum of touched-block sizes
     int32_t heavy[2];                   // round touched a block of > 1 member
+    int32_t csplit[2];                  // the splitter's own block split this round
     int32_t nontriv[2];                 // skip step: least non-trivial candidate
     int32_t skipcnt[2];                 // skip step: rounds retired
     int32_t skip_next[2];               // skip step: splitter after the window
@@ -172,7 +173,7 @@ struct SparseParams {
     int32_t* smin;
     int32_t* kcur;
     int32_t* scur;
-    int32_t* sarr;        // per label: chunks of the block that have tagged (one-pass split)
+    unsigned long long* sarr;  // per label: packed arrival word of the one-pass split (kernels_big.cuh)
     int32_t* splits;
     SCtrl* ctrl;
     GridBarrier* bar;
@@ -185,7 +186,8 @@ struct SparseParams {
     int32_t solo_max_c;         // solo stretches: splitter size and previous-round work
     int32_t solo_max_items;     //   item limits (kernels_loop.cuh)
     int32_t batch_min_c;        // splitter size from which phase A registers blocks in one wave
-    int32_t onepass_major;      // one-pass phase B: CTA-major item placement
+    int32_t onepass_major;      // one-pass phase B: CTA-major item placement up to this many chunks per big block
+    int32_t wide_major;         // ... and the wide layout when its chunks per big block are at most this
     int32_t prefetch_next;      // phase A: prefetch the likely next splitter's member records
     // ---- transition-sharded mode (kernels_shard.cuh); nshard == 1 otherwise
     int32_t nshard;                       // replicas taking part in every round
@@ -232,6 +234,8 @@ __shared__ uint32_t s_u2[32];
 __shared__ int32_t s_nmin;
 __shared__ int32_t s_nsplit;
 __shared__ int32_t s_nmin_round;  // raised minimum of the phase just flushed
+__shared__ int32_t s_csplit;       // this CTA split the splitter's own block this phase
+__shared__ int32_t s_csplit_round;
 
 // Round control of a solo stretch (CTA 0 alone): the registration counters,
 // the successor and its range, the previous round's item count live in
@@ -252,6 +256,7 @@ __device__ __forceinline__ void raise_init() {
         s_nsplit = 0;
         s_ndirty = 0;
         s_nmin_round = 0x7fffffff;
+        s_csplit = s_csplit_round = 0;
         s_ctr_nsmall = 0;
         s_ctr_big = s_ctr_big4 = 0ull;
         s_ctr_heavy = 0;
@@ -279,7 +284,14 @@ __device__ __forceinline__ void u_set(const SparseParams& p, int32_t x) {
 __device__ __forceinline__ void raise_flush_warp0(const SparseParams& p, int cur, int64_t round) {
     const int lane = threadIdx.x & 31;
     const int32_t ns = s_nsplit;
-    if (lane == 0) s_nmin_round = ns ? s_nmin : 0x7fffffff;
+    if (lane == 0) {
+        s_nmin_round = ns ? s_nmin : 0x7fffffff;
+        s_csplit_round = s_csplit;
+        if (s_csplit) {
+            p.ctrl->csplit[cur] = 1;
+            s_csplit = 0;
+        }
+    }
     if (!ns) return;
     const int32_t nd = s_ndirty;
     for (int k = lane; k < nd; k += 32) {
@@ -394,8 +406,23 @@ __device__ int32_t u_next_warp(const SparseParams& p, int32_t from) {
 // lanes of a warp register at once (warp-uniform call): one counter atomic
 // and one `heavy` store per warp instead of one per block -- thousands of
 // blocks are registered per round in the big rounds of c2/c1.
+// What registration reads about block b: its member range and the leader's
+// slot range.  Loaded while the test-and-set is in flight (the arrays only
+// change in phase B).
+struct BlockInfo {
+    int2 r;
+    int32_t ob, nb;
+};
+__device__ __forceinline__ BlockInfo block_info(const SparseParams& p, int32_t b) {
+    BlockInfo i;
+    i.r = p.brange[b];
+    i.ob = p.off ? p.off[b] : b;
+    i.nb = p.off ? p.off[b + 1] - i.ob : 1;
+    return i;
+}
+
 __device__ __forceinline__ void register_blocks_warp(const SparseParams& p, int cur, bool reg, int32_t b,
-                                                     bool solo = false) {
+                                                     BlockInfo bi, bool solo) {
     SCtrl* ctl = p.ctrl;
     // counters: the CTA's shared copies in a solo round, else the global
     // ones (separate code per address space: a generic-pointer atomic costs
@@ -404,9 +431,9 @@ __device__ __forceinline__ void register_blocks_warp(const SparseParams& p, int 
     int2 r = make_int2(0, 0);
     int32_t ob = 0, nb = 0;
     if (reg) {
-        r = p.brange[b];
-        ob = p.off ? p.off[b] : b;
-        nb = p.off ? p.off[b + 1] - ob : 1;
+        r = bi.r;
+        ob = bi.ob;
+        nb = bi.nb;
     }
     const unsigned heavy = __ballot_sync(kFull, reg && r.y > 1);
     if (heavy && lane == __ffs(heavy) - 1) {
@@ -447,8 +474,15 @@ __device__ __forceinline__ void register_blocks_warp(const SparseParams& p, int 
         p.smin[b] = kBig;
         p.kcur[b] = 0;
         p.scur[b] = 0;
-        p.sarr[b] = 0;
+        p.sarr[b] = 0ull;
     }
+}
+
+__device__ __forceinline__ void register_blocks_warp(const SparseParams& p, int cur, bool reg, int32_t b,
+                                                     bool solo = false) {
+    BlockInfo bi{};
+    if (reg) bi = block_info(p, b);
+    register_blocks_warp(p, cur, reg, b, bi, solo);
 }
 
 // Warp-aggregated test-and-set of bit x in bm; returns true in exactly one
@@ -553,6 +587,7 @@ __device__ __forceinline__ void clear_member(const SparseParams& p, int32_t u, b
 
 __device__ __forceinline__ void raise_split(const SparseParams& p, int cur, int64_t round, int32_t l,
                                             int32_t w, int32_t C) {
+    if (l == C) s_csplit = 1;
     u_set(p, l);
     u_set(p, w);
     int32_t lo = min(l, w);
