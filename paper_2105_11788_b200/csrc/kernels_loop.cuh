@@ -28,6 +28,10 @@ constexpr bool kNoCsnap = true;
 #else
 constexpr bool kNoCsnap = false;
 #endif
+#ifndef BISIM_SKIP_GAIN
+#define BISIM_SKIP_GAIN 32
+#endif
+constexpr int32_t kSkipGain = BISIM_SKIP_GAIN;  // rounds a skip step must retire to be retried at once
 constexpr int kA = BISIM_KA;             // in-edges per lane per phase-A step
 
 template <bool IDENT, bool SH>
@@ -217,6 +221,14 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
                 backoff = min(backoff * 2, 4096);
             } else {
                 backoff = 16;
+                // the window stopped at a non-trivial splitter: that round
+                // runs next, so a second try now would retire nothing.  A
+                // try that paid (>= kSkipGain rounds) leaves the next try to
+                // the round's own outcome; a meagre one waits 16 rounds
+                if (nt < lim) {
+                    try_skip = false;
+                    if (retired < kSkipGain) cooldown = 16;
+                }
             }
             continue;
         }

@@ -651,6 +651,10 @@ __device__ int32_t process_small(const SparseParams& p, int cur, int64_t round, 
 // no split, no raised label, no BCRP re-raise (bcrp.py:267-283).  Answers
 // false (the round then runs normally) for splitters of more than 32
 // members or more than kSkipMaxEdges in-edges.
+#ifndef BISIM_TRIV_G
+#define BISIM_TRIV_G 8
+#endif
+constexpr int kTrivG = BISIM_TRIV_G;
 template <bool IDENT>
 __device__ __forceinline__ bool round_is_trivial(const SparseParams& p, int32_t c) {
     const int2 r = p.brange[c];
@@ -661,15 +665,17 @@ __device__ __forceinline__ bool round_is_trivial(const SparseParams& p, int32_t 
         const int32_t e0 = mr.z, e1 = mr.w;
         if (e1 - e0 > budget) return false;
         budget -= e1 - e0;
-        for (int32_t e = e0; e < e1; e += 4) {
-            int32_t s[4], b[4];
+        // kTrivG in-edges per step: their three dependent loads (reverse
+        // edge, source block, block size) go out together
+        for (int32_t e = e0; e < e1; e += kTrivG) {
+            int32_t s[kTrivG], b[kTrivG];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) s[k] = e + k < e1 ? (IDENT ? p.rev_src[e + k] : p.rev[e + k].y) : -1;
+            for (int k = 0; k < kTrivG; ++k) s[k] = e + k < e1 ? (IDENT ? p.rev_src[e + k] : p.rev[e + k].y) : -1;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) b[k] = s[k] >= 0 ? p.block[s[k]] : -1;
+            for (int k = 0; k < kTrivG; ++k) b[k] = s[k] >= 0 ? p.block[s[k]] : -1;
             bool single = true;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) single &= b[k] < 0 || p.brange[b[k]].y == 1;
+            for (int k = 0; k < kTrivG; ++k) single &= b[k] < 0 || p.brange[b[k]].y == 1;
             if (!single) return false;
         }
     }
