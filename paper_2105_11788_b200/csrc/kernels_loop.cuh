@@ -16,9 +16,10 @@
 // warp count) and the phase barrier differ, so rounds are bit-identical.
 #pragma once
 
-// measured on c1 / c2 (512-thread CTAs): 16 / 128 beat 64 / 64 by 6 / 3 %
-constexpr int32_t kSoloMaxC = 16;
-constexpr int32_t kSoloMaxItems = 128;
+// measured on c1 / c2 (512-thread CTAs): 16 / 128 beat 64 / 64 by 6 / 3 %;
+// after the skip-step change 32 / 256 beat 16 / 128 by 4.3 / 0.5 %
+constexpr int32_t kSoloMaxC = 32;
+constexpr int32_t kSoloMaxItems = 256;
 constexpr int32_t kSoloSkipSpan = 512;   // skip-step window of the solo team: one label per thread
 #ifndef BISIM_KA
 #define BISIM_KA 2
