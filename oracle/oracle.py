@@ -79,6 +79,13 @@ def lib():
         L.oracle_rcpp.argtypes = [ctypes.c_int32, ctypes.c_int64, i32p, i32p, i32p,
                                   ctypes.c_int64, i32p, i32p, ctypes.c_int64, i32p,
                                   ctypes.c_int64, ctypes.c_int64, P(_Stats), ctypes.c_int]
+        L.oracle_bcrp_fast.restype = ctypes.c_int
+        L.oracle_bcrp_fast.argtypes = [ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, i32p, i32p,
+                                       i32p, ctypes.c_int64, i32p, i32p, ctypes.c_int64,
+                                       P(_Stats), ctypes.c_int]
+        L.oracle_rcpp_fast.restype = ctypes.c_int
+        L.oracle_rcpp_fast.argtypes = [ctypes.c_int32, ctypes.c_int64, i32p, i32p, i32p,
+                                       ctypes.c_int64, i32p, i32p, ctypes.c_int64, P(_Stats)]
         _lib = L
     return _lib
 
@@ -116,6 +123,33 @@ def label_partition(n, src, act, num_actions, threads=1) -> np.ndarray:
     if rc != OR_OK:
         raise RuntimeError(f"oracle label partition failed ({rc})")
     return block
+
+
+def bcrp_fast(n, src, act, dst, num_actions, max_supersteps=None, threads=1) -> OracleResult:
+    """Event-driven sequential restatement (oracle/bisim_fast.c): same
+    results as bcrp(), round cost O(|C| + in(C) + touched blocks)."""
+    src, act, dst = _i32(src), _i32(act), _i32(dst)
+    guard = _DEFAULT_GUARD if max_supersteps is None else int(max_supersteps)
+    cap = 3 * n + num_actions + 9 if max_supersteps is None else max(int(max_supersteps), 0) + 1
+    block = np.empty(n, np.int32)
+    splits = np.zeros(cap + 1, np.int32)
+    st = _Stats()
+    rc = lib().oracle_bcrp_fast(n, src.size, num_actions, _ptr(src), _ptr(act), _ptr(dst), guard,
+                                _ptr(block), _ptr(splits), cap, ctypes.byref(st), threads)
+    return _finish(rc, st, block, splits, None, 0)
+
+
+def rcpp_fast(n, src, dst, pi0, max_supersteps=None) -> OracleResult:
+    """Event-driven sequential restatement of rcpp() (oracle/bisim_fast.c)."""
+    src, dst, pi0 = _i32(src), _i32(dst), _i32(pi0)
+    guard = _DEFAULT_GUARD if max_supersteps is None else int(max_supersteps)
+    cap = 3 * n + 10 if max_supersteps is None else max(int(max_supersteps), 0) + 1
+    block = np.empty(n, np.int32)
+    splits = np.zeros(cap + 1, np.int32)
+    st = _Stats()
+    rc = lib().oracle_rcpp_fast(n, src.size, _ptr(src), _ptr(dst), _ptr(pi0), guard, _ptr(block),
+                                _ptr(splits), cap, ctypes.byref(st))
+    return _finish(rc, st, block, splits, None, 0)
 
 
 def _finish(rc, st, block, splits, snap, snap_rounds):
