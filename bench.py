@@ -7,13 +7,18 @@ A step is one complete coarsest-partition computation (preprocessing, label
 pre-partition, refinement loop) of one synthetic LTS.  Default workload:
 config c5 -- a VLTS-shaped lifted-quotient LTS with n = 10M
 states, m = 100M transitions, |Act| = 32, one independent instance per GPU
-(seed = rank), so the job weak-scales with no data-path collective.
+(seed = rank), so the job weak-scales with no data-path collective.  With
+--gpus N > 1 and no launcher, bench.py relaunches itself under
+torch.distributed.run (one process per GPU).
 
 `value` = (n+m) x K x N / max-over-ranks device time of K steps with inputs
 resident in HBM (CUDA events on the library's stream).  `e2e` = the same
-metric through the host C-ABI entry point (bisim_bcrp: pinned host arrays
-in, H2D + D2H inside the timed region).  `--impl reference` times the CPU
-oracle port of the reference algorithm on the same workload (rank 0 only).
+metric through the host C-ABI entry point (bisim_bcrp_ex: pinned host arrays
+in, H2D + D2H inside the timed region); `e2e_api` = through the public
+Python call bcrp_arrays with ordinary numpy arrays.  The result is checked
+against the RunStats and block digest of a CPU-oracle run to completion
+(tests/golden/scale/).  `--impl reference` times the CPU oracle port of the
+reference algorithm on the same workload (rank 0 only; see CpuSampler).
 """
 from __future__ import annotations
 
@@ -35,11 +40,37 @@ sys.path.insert(0, ROOT)
 METRIC = "(n+m)/s to coarsest partition"
 UNIT = "(n+m)/s"
 
-# Round counts of the default-seed workloads, measured by the GPU path and
-# pinned by tests/test_bench_contract.py; the CPU reference arm extrapolates
-# its sampled per-round time with them.
-KNOWN_SUPERSTEPS = {"c5": 6113, "c1": 13962, "c2": 1201621, "c3": 399998, "c4u": 5006404,
-                    "c4l": 24344}
+SCALE_FIXTURES = os.path.join(ROOT, "tests", "golden", "scale")
+
+
+def oracle_runstats(config: str):
+    """RunStats of the seed-0 instance of `config` from a CPU-oracle run to
+    completion (tests/golden/scale/, oracle/gen_scale.py) -- the round count
+    the reference arm extrapolates with, and the GPU result's check."""
+    path = os.path.join(SCALE_FIXTURES, f"{config}.fast.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except OSError:
+        return None
+
+
+def config_dict(config: str, inst, desc: str, world: int) -> dict:
+    """The `config` object both arms print (identical by construction)."""
+    rec = oracle_runstats(config) or {}
+    return {"workload": desc, "n": inst.n, "m": inst.m, "num_actions": inst.num_actions,
+            "kind": inst.kind, "supersteps": rec.get("supersteps"),
+            "initial_blocks": rec.get("initial_blocks"), "final_blocks": rec.get("final_blocks"),
+            "parallelism": f"replicas x{world} (one independent LTS per GPU)",
+            "l2": _l2_note(inst)}
+
+
+def _l2_note(inst) -> str:
+    w = 12 if inst.kind == "bcrp" else 8
+    gb = w * inst.m / 1e9
+    if gb > 0.126:
+        return "inputs (%d B x m = %.2f GB) exceed the 126 MB L2; no flush" % (w, gb)
+    return "inputs (%d B x m = %.1f MB) fit in L2 (small config; no flush)" % (w, gb * 1e3)
 
 
 def make_instance(config: str, rank: int):
@@ -127,66 +158,111 @@ def measured_peak_hbm():
         return 6650.0, "fallback"
 
 
-def cpu_sample(inst, supersteps: int, budget_s: float = 20.0):
-    """Time the oracle port (all host threads) on a bounded sample of the
-    workload: preprocessing + label/pi0 setup + K main-loop rounds, then
-    extrapolate to R = `supersteps` rounds."""
-    from oracle import oracle
-    threads = os.cpu_count() or 1
-    kw = dict(threads=threads)
-    probe = 2
-    t0 = time.perf_counter()
-    if inst.kind == "bcrp":
-        r = oracle.bcrp(inst.n, inst.src, inst.act, inst.dst, inst.num_actions, stop_after=probe, **kw)
-    else:
-        r = oracle.rcpp(inst.n, inst.src, inst.dst, inst.pi0, stop_after=probe, **kw)
-    wall = time.perf_counter() - t0
-    per_round = r.t_loop_s / max(r.supersteps, 1)
-    K = max(probe, min(supersteps, int(max(budget_s - wall, 0) / max(per_round, 1e-9))))
-    if K > probe:
-        if inst.kind == "bcrp":
-            r = oracle.bcrp(inst.n, inst.src, inst.act, inst.dst, inst.num_actions, stop_after=K, **kw)
-        else:
-            r = oracle.rcpp(inst.n, inst.src, inst.dst, inst.pi0, stop_after=K, **kw)
-        per_round = r.t_loop_s / max(r.supersteps, 1)
-    done = r.supersteps
-    t_est = r.t_pre_s + r.t_label_s + per_round * supersteps
-    exact = done >= supersteps
-    sample = (f"oracle port (oracle/bisim_oracle.c, OpenMP {threads} threads): preprocessing + "
-              f"{'label pre-partition' if inst.kind == 'bcrp' else 'pi0 setup'} + {done} of "
-              f"{supersteps} main-loop rounds timed; "
-              + ("complete run" if exact else
-                 f"total extrapolated as t_pre + t_label + R x {per_round * 1e3:.3f} ms/round"))
-    return (inst.n + inst.m) / t_est, t_est, threads, sample
+class CpuSampler:
+    """The reference algorithm on the host cores (oracle port, all threads),
+    timed on a bounded sample of the workload.
+
+    Setup -- preprocessing and the label pre-partition (BCRP) or pi0 (RCPP)
+    -- runs once and is timed once.  Main-loop rounds are timed in windows
+    of `window` rounds that start at the beginning, the middle and the end
+    of the run: the literal oracle resumes from the program state the
+    event-driven oracle reports after round r0 (oracle.fast_states, untimed
+    setup).  The estimate of one complete run is t_pre + t_label + R x
+    (mean of the windows' ms/round), with R the round count of the oracle's
+    own complete run (tests/golden/scale/).
+    """
+
+    def __init__(self, config: str, inst, window: int):
+        from oracle import oracle
+        # all host threads, except where OpenMP fork/join per phase would
+        # cost more than the phase (small systems run fastest on one core)
+        self.threads = max(1, min(os.cpu_count() or 1, (inst.n + inst.m) // 250_000))
+        rec = oracle_runstats(config)
+        if rec is None:
+            raise SystemExit(f"bench: no oracle fixture for {config} (oracle/gen_scale.py)")
+        self.R = int(rec["supersteps"])
+        self.window = max(1, min(window, self.R))
+        self.run = oracle.OracleRun(inst, self.threads)
+        block0 = self.run.block()
+        unstable0 = np.zeros(inst.n, np.uint8)
+        unstable0[block0] = 1
+        starts = [0, self.R // 2, max(self.R - self.window, 0)]
+        later = sorted({r for r in starts if r > 0})
+        states = oracle.fast_states(inst, later, threads=self.threads) if later else ([], [])
+        by_round = {r: (states[0][i], states[1][i]) for i, r in enumerate(later)}
+        by_round[0] = (block0, unstable0)
+        self.windows = [(r, by_round[r]) for r in starts]
+        self.samples = {r: [] for r in starts}  # seconds per round, per window
+
+    def step(self, i: int) -> float:
+        """Time one window (cycling start / middle / end); returns seconds."""
+        r0, (block, unstable) = self.windows[i % len(self.windows)]
+        self.run.set_state(block, unstable)
+        k, sec = self.run.rounds(min(self.window, self.R - r0))
+        if k:
+            self.samples[r0].append(sec / k)
+        return sec
+
+    def estimate(self):
+        per = [statistics.mean(v) for v in self.samples.values() if v]
+        per_round = statistics.mean(per)
+        t = self.run.t_pre_s + self.run.t_label_s + self.R * per_round
+        rounds = sum(len(v) for v in self.samples.values()) * self.window
+        desc = (f"oracle port (oracle/bisim_oracle.c, literal O(n+m) rounds, OpenMP "
+                f"{self.threads} threads): setup (preprocessing + "
+                f"label pre-partition / pi0) timed once = {self.run.t_pre_s + self.run.t_label_s:.2f} s; "
+                f"{rounds} main-loop rounds timed in windows of {self.window} at rounds "
+                f"{', '.join(str(r + 1) for r, _ in self.windows)} of R = {self.R} "
+                f"({', '.join('%.3f' % (statistics.mean(v) * 1e3) for v in self.samples.values() if v)}"
+                f" ms/round); total extrapolated as t_setup + R x mean ms/round")
+        return t, per_round, desc
+
+    def close(self):
+        self.run.close()
+
+
+def cpu_baseline(config: str, inst, window: int = 70) -> dict:
+    """cpu_baseline of the GPU arm's line (rank 0, N=1): three windows."""
+    cs = CpuSampler(config, inst, window)
+    try:
+        for i in range(3):
+            cs.step(i)
+        t, per_round, desc = cs.estimate()
+    finally:
+        cs.close()
+    return {"value": (inst.n + inst.m) / t, "unit": UNIT, "cores": cs.threads, "kind": "port",
+            "sample": desc, "t_total_s": t, "ms_per_round": per_round * 1e3}
 
 
 def run_reference(args):
+    """Reference arm: the reference algorithm (oracle port) on the host cores,
+    same workload, config and metric as the GPU arm; rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
     inst, desc = make_instance(args.config, 0)
-    R = KNOWN_SUPERSTEPS.get(args.config)
-    if R is None:
-        from oracle import oracle
-        if inst.kind == "bcrp":
-            R = oracle.bcrp(inst.n, inst.src, inst.act, inst.dst, inst.num_actions,
-                            threads=os.cpu_count()).supersteps
-        else:
-            R = oracle.rcpp(inst.n, inst.src, inst.dst, inst.pi0, threads=os.cpu_count()).supersteps
-    vals, times = [], []
-    for step in range(args.warmup + args.steps):
-        v, t, cores, sample = cpu_sample(inst, R, budget_s=args.cpu_budget)
-        if step >= args.warmup:
-            vals.append(v)
-            times.append(t)
-    value = statistics.mean(vals)
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.mean(times) * 1e3,
+    steps_total = args.warmup + args.steps
+    # >= 210 timed rounds over the K timed steps, windows cycling start/middle/end
+    window = max(10, -(-210 // max(args.steps, 1)))
+    cs = CpuSampler(args.config, inst, window)
+    try:
+        for i in range(steps_total):
+            if i == args.warmup:
+                for v in cs.samples.values():
+                    v.clear()
+            cs.step(i)
+        t, per_round, sample = cs.estimate()
+    finally:
+        cs.close()
+    value = (inst.n + inst.m) / t
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
-            "data": "synthetic", "config": {"workload": desc, "n": inst.n, "m": inst.m,
-                                            "supersteps": R},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+            "data": "synthetic", "config": config_dict(args.config, inst, desc, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cs.threads, "kind": "port",
                              "sample": sample},
+            "ms_per_round": per_round * 1e3,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -210,22 +286,22 @@ def job_throughput(units_per_rank: int, steps: int, world: int, ms_max: float) -
     return units_per_rank * steps * world / (ms_max / 1e3)
 
 
-def empty_round_floor_us(device: int, n: int = 20000) -> float:
+def empty_round_floors_us(device: int, n: int = 20000) -> dict:
     """Latency floor of one refinement round: RCPP on an edge-free system
     with a discrete pi0 runs n rounds whose splitter has no in-edge (pure
-    control + barriers); no-op retirement disabled so every round runs."""
+    control), one by one (no bulk retirement).  `solo`: such rounds run on
+    one CTA with __syncthreads (the schedule small rounds get); `grid`: every
+    round on the whole grid with its two grid barriers (the schedule c5's
+    rounds pay)."""
+    from paper_2105_11788_b200 import _native as N
     from paper_2105_11788_b200 import rcpp_arrays
-    old = os.environ.get("BISIM_NO_SKIP")
-    os.environ["BISIM_NO_SKIP"] = "1"
-    try:
-        empty = np.zeros(0, np.int32)
-        _, st, ns = rcpp_arrays(n, empty, empty, np.arange(n, dtype=np.int32), device=device)
-    finally:
-        if old is None:
-            del os.environ["BISIM_NO_SKIP"]
-        else:
-            os.environ["BISIM_NO_SKIP"] = old
-    return ns["t_alg_ms"] * 1e3 / max(st.supersteps, 1)
+    empty = np.zeros(0, np.int32)
+    out = {}
+    for name, flags in (("solo", N.FLAG_NO_SKIP), ("grid", N.FLAG_NO_SKIP | N.FLAG_NO_SOLO)):
+        _, st, ns = rcpp_arrays(n, empty, empty, np.arange(n, dtype=np.int32), device=device,
+                                flags=flags)
+        out[name] = ns["t_alg_ms"] * 1e3 / max(st.supersteps, 1)
+    return out
 
 
 def run_b200(args):
@@ -306,20 +382,28 @@ def run_b200(args):
             dist.barrier()
         return reduce_max(e0.elapsed_time(e1), dev), sts
 
-    # warm-up + correctness check against the known coarsest partition
+    # warm-up + correctness: the coarsest partition and RunStats of the
+    # oracle's complete run (tests/golden/scale/) or the analytic truth
     first = None
     for _ in range(args.warmup):
         first = step_device()
     if first is None:
         first = step_device()
     blk = d_block.cpu().numpy()
-    correct = None
+    parity = {}
     if inst.truth is not None:
-        correct = bool(np.array_equal(blk, inst.truth))
-    if inst.expect_supersteps is not None:
-        correct = (correct is not False) and first.supersteps == inst.expect_supersteps
-    if correct is False:
-        raise SystemExit("bench: GPU result differs from the known coarsest partition")
+        parity["vs_truth"] = bool(np.array_equal(blk, inst.truth))
+    rec = oracle_runstats(args.config) if rank == 0 else None
+    if rec is not None:
+        import hashlib
+        sha = lambda a: hashlib.sha256(np.ascontiguousarray(a, dtype="<i4").tobytes()).hexdigest()
+        R0 = int(first.supersteps)
+        parity["vs_oracle_runstats"] = bool(
+            R0 == rec["supersteps"] and first.initial_blocks == rec["initial_blocks"]
+            and first.final_blocks == rec["final_blocks"] and sha(blk) == rec["block_sha256"]
+            and sha(splits[:R0]) == rec["splits_sha256"])
+    if False in parity.values():
+        raise SystemExit(f"bench: GPU result differs from the reference program ({parity})")
 
     with ClockSampler(local) as clocks:
         ms, sts = timed(step_device, args.steps)
@@ -330,7 +414,25 @@ def run_b200(args):
     if inst.truth is not None and not np.array_equal(h_block, inst.truth):
         raise SystemExit("bench: host-path result differs from the known coarsest partition")
 
-    floor_us = empty_round_floor_us(local) if rank == 0 else None
+    # e2e through the public Python API with ordinary (pageable) numpy arrays
+    from paper_2105_11788_b200 import bcrp_arrays, rcpp_arrays
+
+    def step_api():
+        if inst.kind == "bcrp":
+            return bcrp_arrays(n, inst.src, inst.act, inst.dst, inst.num_actions, device=local)
+        return rcpp_arrays(n, inst.src, inst.dst, inst.pi0, device=local)
+
+    step_api()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        blk_api = step_api()[0]
+    ms_api = reduce_max((time.perf_counter() - t0) * 1e3, dev)
+    if inst.truth is not None and not np.array_equal(blk_api, inst.truth):
+        raise SystemExit("bench: public-API result differs from the known coarsest partition")
+
+    floors = empty_round_floors_us(local) if rank == 0 else None
 
     R = sts[0].supersteps
     value = job_throughput(n + m, args.steps, world, ms)
@@ -340,14 +442,14 @@ def run_b200(args):
     peak, peak_kind = measured_peak_hbm()
     achieved = bytes_alg / (t_alg / 1e3) / 1e9
     launches = sum(s.kernel_launches for s in sts)
+    h2d = int(4 * m * (3 if inst.kind == "bcrp" else 2) + (4 * n if inst.kind == "rcpp" else 0))
+    d2h = int(4 * n + 4 * R)
 
     result = None
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu:
-            v, t_est, cores, sample = cpu_sample(inst, R, budget_s=args.cpu_budget)
-            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
-                   "t_total_s": t_est}
+            cpu = cpu_baseline(args.config, inst)
         traffic = None
         prof = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
         if os.path.exists(prof):
@@ -357,24 +459,22 @@ def run_b200(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": desc, "n": n, "m": m, "num_actions": inst.num_actions,
-                       "kind": inst.kind, "supersteps": R,
-                       "initial_blocks": sts[0].initial_blocks,
-                       "final_blocks": sts[0].final_blocks,
-                       "parallelism": f"replicas x{world} (one independent LTS per GPU)",
-                       "l2": "inputs (12 B x m = %.2f GB) exceed L2; no flush" % (12 * m / 1e9),
-                       "correct_vs_truth": correct},
+            "config": config_dict(args.config, inst, desc, world),
+            "parity": parity,
             "ms_to_partition": ms / args.steps,
             "phase_ms": {"pre": statistics.mean(s.t_pre_ms for s in sts),
                          "label": statistics.mean(s.t_label_ms for s in sts),
                          "alg": t_alg},
             "per_round_us": t_alg * 1e3 / max(R, 1),
-            "per_round_floor_us": floor_us,
+            "per_round_floor_us": floors,
             "rounds_retired": sts[0].rounds_retired,
             "e2e": {"value": e2e, "unit": UNIT, "ms_per_step": ms_e2e / args.steps,
-                    "h2d_bytes_per_step": int(4 * m * (3 if inst.kind == "bcrp" else 2)
-                                              + (4 * n if inst.kind == "rcpp" else 0)),
-                    "d2h_bytes_per_step": int(4 * n + 4 * R)},
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "path": "C ABI bisim_bcrp_ex/bisim_rcpp_ex, pinned host arrays, CUDA events"},
+            "e2e_api": {"value": job_throughput(n + m, args.steps, world, ms_api), "unit": UNIT,
+                        "ms_per_step": ms_api / args.steps, "h2d_bytes_per_step": h2d,
+                        "d2h_bytes_per_step": d2h,
+                        "path": "bcrp_arrays/rcpp_arrays, pageable numpy arrays, wall clock"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "k_refine_sparse (persistent refinement loop)",
@@ -458,6 +558,13 @@ def run_sharded_bench(args):
     return 0
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -469,9 +576,17 @@ def main():
     ap.add_argument("--virtual", type=int, default=0,
                     help="with --sharded: this many replicas sharing GPU 0 (testing)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     args = ap.parse_args()
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and args.gpus > 1 and not args.sharded:
+        # one process per GPU: relaunch under torch.distributed.run
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
+    if world is not None and int(world) != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         return run_reference(args)
     if args.sharded:

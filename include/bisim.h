@@ -82,11 +82,21 @@ typedef struct bisim_stats {
  * non-zero return aborts the run with BISIM_ABORTED. */
 typedef int (*bisim_observer_fn)(int64_t iteration, const int32_t *block, int32_t n, void *user);
 
+/* Loop-variant flags (bisim_options.flags).  None changes a result: each
+ * selects another schedule of the same Priority program, and the parity
+ * tests run every variant against the oracle. */
+#define BISIM_FLAG_NO_SKIP 1u              /* run no-op rounds one by one (no bulk retirement) */
+#define BISIM_FLAG_NO_SOLO 2u              /* every round on the whole grid (no CTA-solo stretches) */
+#define BISIM_FLAG_CTA_MAJOR 4u            /* phase-B work items CTA-major */
+#define BISIM_FLAG_LITERAL_LABEL_ROUNDS 8u /* label pre-partition as |Act| literal rounds */
+
 typedef struct bisim_options {
     int32_t device;          /* CUDA ordinal */
     int32_t mode;            /* BISIM_MODE_* */
     bisim_observer_fn observer;
     void *observer_user;
+    uint32_t flags;          /* BISIM_FLAG_* (0 = default schedule) */
+    int32_t reserved;
 } bisim_options;
 
 /* ---- host-pointer entry points (the reference-facing boundary) ---------- */
@@ -150,7 +160,22 @@ int bisim_preprocess(int32_t n, int64_t m, int32_t num_actions, const int32_t *s
                      const int32_t *act, int32_t *order_out, int32_t *nr_marks_out,
                      int32_t *off_out, int64_t *mark_length, int device);
 
-/* partition_by_outgoing_labels(lts, Priority) (bcrp.py:129-141). */
+/* preprocess(lts) -> BcrpAux in the reference's layout (bcrp.py:116-126):
+ * the transitions stably sorted by (source, action) (bcrp.py:49-52; GPU
+ * radix sort), perm_out[k] = original index of sorted transition k, the
+ * sorted columns, action_switch_out[k] (bcrp.py:55-65) and order_out[k]
+ * (bcrp.py:91-104) per SORTED transition, nr_marks_out[s] and off_out[s]
+ * (exclusive scan, bcrp.py:105-112) per state, *mark_length = L.  Any
+ * output pointer may be NULL.  Host pointers. */
+int bisim_preprocess_sorted(int32_t n, int64_t m, int32_t num_actions, const int32_t *src,
+                            const int32_t *act, const int32_t *dst, int32_t *perm_out,
+                            int32_t *src_out, int32_t *act_out, int32_t *dst_out,
+                            int32_t *action_switch_out, int32_t *order_out,
+                            int32_t *nr_marks_out, int32_t *off_out, int64_t *mark_length,
+                            int device);
+
+/* partition_by_outgoing_labels(lts, Priority) (bcrp.py:129-141): only the
+ * label kernels run (validation, label sets, canonical grouping). */
 int bisim_label_partition(int32_t n, int64_t m, int32_t num_actions, const int32_t *src,
                           const int32_t *act, int32_t *block_out, int device);
 

@@ -168,7 +168,8 @@ static void parts_split(parts *P, int32_t b, const int32_t *splist, int32_t k, i
 static int refine(int32_t n, int bcrp, const int32_t *off, const int32_t *nr,
                   const int32_t *rin_ptr, const int32_t *rin_slot, const int32_t *rin_src,
                   int64_t mark_len, int32_t *block, int64_t max_supersteps, int64_t steps0,
-                  int32_t *splits_out, int64_t splits_cap, oracle_stats *st) {
+                  int32_t *splits_out, int64_t splits_cap, oracle_stats *st,
+                  int64_t nstop, const int64_t *stops, int32_t *blocks_out, uint8_t *unstable_out) {
     int rc = OR_NOMEM;
     parts P;
     memset(&P, 0, sizeof P);
@@ -240,7 +241,19 @@ static int refine(int32_t n, int bcrp, const int32_t *off, const int32_t *nr,
         if (bcrp && nsplit > 0) heap_push(&q, C); /* bcrp.py:282 */
         for (int64_t i = 0; i < nmarked; ++i) mark[marked[i]] = 0;
         if (splits_out && rounds <= splits_cap) splits_out[rounds - 1] = nsplit;
+        /* checkpoints: the program's state (block, unstable) after round
+         * stops[i] -- what the literal oracle resumes from (oracle_set_state) */
+        while (nstop > 0 && stops[0] == rounds) {
+            memcpy(blocks_out, block, (size_t)n * 4);
+            memcpy(unstable_out, q.flag, (size_t)n);
+            blocks_out += n;
+            unstable_out += n;
+            ++stops;
+            --nstop;
+            if (nstop == 0) goto done;
+        }
     }
+done:
     st->supersteps = rounds;
     rc = OR_OK;
 out:
@@ -277,9 +290,11 @@ static int build_rin(int32_t n, int64_t m, const int32_t *esrc, const int32_t *e
     return OR_OK;
 }
 
-int oracle_bcrp_fast(int32_t n, int64_t m, int32_t A, const int32_t *src, const int32_t *act,
+static int bcrp_fast(int32_t n, int64_t m, int32_t A, const int32_t *src, const int32_t *act,
                      const int32_t *dst, int64_t max_supersteps, int32_t *block_out,
-                     int32_t *splits_out, int64_t splits_cap, oracle_stats *st, int threads) {
+                     int32_t *splits_out, int64_t splits_cap, oracle_stats *st, int threads,
+                     int64_t nstop, const int64_t *stops, int32_t *blocks_out,
+                     uint8_t *unstable_out) {
     memset(st, 0, sizeof(*st));
     if (n < 1 || m < 0 || A < 0) return OR_BAD_INPUT;
     for (int64_t i = 0; i < m; ++i)
@@ -323,7 +338,7 @@ int oracle_bcrp_fast(int32_t n, int64_t m, int32_t A, const int32_t *src, const 
     double t2 = fnow();
     st->t_label_s = t2 - t1;
     rc = refine(n, 1, off, nr, rptr, rslot, rsrc, L, block_out, max_supersteps, A, splits_out,
-                splits_cap, st);
+                splits_cap, st, nstop, stops, blocks_out, unstable_out);
     st->t_loop_s = fnow() - t2;
     if (rc == OR_OK) st->final_blocks = nblocks(n, block_out);
 out:
@@ -332,9 +347,11 @@ out:
     return rc;
 }
 
-int oracle_rcpp_fast(int32_t n, int64_t m, const int32_t *src, const int32_t *dst,
+static int rcpp_fast(int32_t n, int64_t m, const int32_t *src, const int32_t *dst,
                      const int32_t *pi0, int64_t max_supersteps, int32_t *block_out,
-                     int32_t *splits_out, int64_t splits_cap, oracle_stats *st) {
+                     int32_t *splits_out, int64_t splits_cap, oracle_stats *st,
+                     int64_t nstop, const int64_t *stops, int32_t *blocks_out,
+                     uint8_t *unstable_out) {
     memset(st, 0, sizeof(*st));
     if (n < 1 || m < 0) return OR_BAD_INPUT;
     for (int64_t i = 0; i < m; ++i)
@@ -356,10 +373,43 @@ int oracle_rcpp_fast(int32_t n, int64_t m, const int32_t *src, const int32_t *ds
     double t2 = fnow();
     st->t_label_s = t2 - t0;
     rc = refine(n, 0, off, nr, rptr, rslot, rsrc, n, block_out, max_supersteps, 0, splits_out,
-                splits_cap, st);
+                splits_cap, st, nstop, stops, blocks_out, unstable_out);
     st->t_loop_s = fnow() - t2;
     if (rc == OR_OK) st->final_blocks = nblocks(n, block_out);
 out:
     free(off); free(nr); free(rptr); free(rslot); free(rsrc);
+    return rc;
+}
+
+int oracle_bcrp_fast(int32_t n, int64_t m, int32_t A, const int32_t *src, const int32_t *act,
+                     const int32_t *dst, int64_t max_supersteps, int32_t *block_out,
+                     int32_t *splits_out, int64_t splits_cap, oracle_stats *st, int threads) {
+    return bcrp_fast(n, m, A, src, act, dst, max_supersteps, block_out, splits_out, splits_cap, st,
+                     threads, 0, NULL, NULL, NULL);
+}
+
+int oracle_rcpp_fast(int32_t n, int64_t m, const int32_t *src, const int32_t *dst,
+                     const int32_t *pi0, int64_t max_supersteps, int32_t *block_out,
+                     int32_t *splits_out, int64_t splits_cap, oracle_stats *st) {
+    return rcpp_fast(n, m, src, dst, pi0, max_supersteps, block_out, splits_out, splits_cap, st, 0,
+                     NULL, NULL, NULL);
+}
+
+/* States (block, unstable flags) of the reference program after rounds
+ * stops[0] < stops[1] < ... (nstop of them, each <= the run's length):
+ * blocks_out / unstable_out hold nstop * n entries.  bench.py uses them to
+ * time the literal oracle on windows from the middle and end of a run. */
+int oracle_fast_states(int bcrp, int32_t n, int64_t m, int32_t A, const int32_t *src,
+                       const int32_t *act, const int32_t *dst, const int32_t *pi0, int64_t nstop,
+                       const int64_t *stops, int32_t *blocks_out, uint8_t *unstable_out,
+                       int threads) {
+    oracle_stats st;
+    int32_t *block = malloc((size_t)n * 4);
+    if (!block) return OR_NOMEM;
+    int rc = bcrp ? bcrp_fast(n, m, A, src, act, dst, -1, block, NULL, 0, &st, threads, nstop,
+                              stops, blocks_out, unstable_out)
+                  : rcpp_fast(n, m, src, dst, pi0, -1, block, NULL, 0, &st, nstop, stops,
+                              blocks_out, unstable_out);
+    free(block);
     return rc;
 }

@@ -42,7 +42,7 @@ def sha(a) -> str:
     return hashlib.sha256(np.ascontiguousarray(a, dtype="<i4").tobytes()).hexdigest()
 
 
-def run(config: str, which: str, threads: int) -> dict:
+def run(config: str, which: str, threads: int, signature: bool = False) -> dict:
     import bench
     from oracle import oracle
     inst, desc = bench.make_instance(config, 0)
@@ -66,6 +66,14 @@ def run(config: str, which: str, threads: int) -> dict:
            "splits_sha256": sha(r.splits), "splits_sum": int(np.asarray(r.splits, np.int64).sum()),
            "block_sha256": sha(r.block), "threads": threads, "wall_s": round(wall, 1),
            "truth_equal": None if inst.truth is None else bool(np.array_equal(r.block, inst.truth))}
+    if signature and inst.truth is None:
+        # an independent fixed point (iterated signature refinement,
+        # workloads.signature_bisim) for configs without an analytic truth
+        from paper_2105_11788_b200 import workloads as W
+        act = inst.act if inst.kind == "bcrp" else np.zeros(inst.m, np.int32)
+        truth = W.signature_bisim(inst.n, inst.src, act, inst.dst,
+                                  init=None if inst.kind == "bcrp" else inst.pi0)
+        rec["signature_equal"] = bool(np.array_equal(r.block, truth))
     os.makedirs(OUT, exist_ok=True)
     base = os.path.join(OUT, f"{config}.{which}")
     np.savez_compressed(base + ".npz", splits=np.asarray(r.splits, np.int32))
@@ -78,10 +86,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--oracle", choices=["literal", "fast"], default="fast")
     ap.add_argument("--threads", type=int, default=os.cpu_count() or 1)
+    ap.add_argument("--signature", action="store_true",
+                    help="also record equality with the signature-refinement fixed point")
     ap.add_argument("configs", nargs="+")
     a = ap.parse_args()
     for c in a.configs:
-        rec = run(c, a.oracle, a.threads)
+        rec = run(c, a.oracle, a.threads, a.signature)
         print(json.dumps(rec), flush=True)
 
 

@@ -86,6 +86,24 @@ def lib():
         L.oracle_rcpp_fast.restype = ctypes.c_int
         L.oracle_rcpp_fast.argtypes = [ctypes.c_int32, ctypes.c_int64, i32p, i32p, i32p,
                                        ctypes.c_int64, i32p, i32p, ctypes.c_int64, P(_Stats)]
+        vp = ctypes.c_void_p
+        u8p = P(ctypes.c_uint8)
+        i64p = P(ctypes.c_int64)
+        L.oracle_open.restype = vp
+        L.oracle_open.argtypes = [ctypes.c_int, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32,
+                                  i32p, i32p, i32p, i32p, ctypes.c_int, P(_Stats)]
+        L.oracle_set_state.restype = None
+        L.oracle_set_state.argtypes = [vp, i32p, u8p]
+        L.oracle_rounds.restype = ctypes.c_int64
+        L.oracle_rounds.argtypes = [vp, ctypes.c_int64, ctypes.c_int, P(ctypes.c_double)]
+        L.oracle_block.restype = i32p
+        L.oracle_block.argtypes = [vp]
+        L.oracle_close.restype = None
+        L.oracle_close.argtypes = [vp]
+        L.oracle_fast_states.restype = ctypes.c_int
+        L.oracle_fast_states.argtypes = [ctypes.c_int, ctypes.c_int32, ctypes.c_int64,
+                                         ctypes.c_int32, i32p, i32p, i32p, i32p, ctypes.c_int64,
+                                         i64p, i32p, u8p, ctypes.c_int]
         _lib = L
     return _lib
 
@@ -197,3 +215,74 @@ def rcpp(n, src, dst, pi0, max_supersteps=None, snap_rounds=0, threads=1,
                            _ptr(splits), cap, _ptr(snap) if snap is not None else None,
                            snap_rounds, stop_after, ctypes.byref(st), threads)
     return _finish(rc, st, block, splits, snap, snap_rounds)
+
+
+class OracleRun:
+    """Literal oracle with setup done once (timed once) and the main loop
+    resumable from any reachable state: bench.py times windows of rounds from
+    the start, middle and end of a run this way (see fast_states)."""
+
+    def __init__(self, inst, threads: int):
+        self.threads = threads
+        self.bcrp = inst.kind == "bcrp"
+        self.n = inst.n
+        self._keep = [_i32(inst.src), _i32(inst.dst)]
+        if self.bcrp:
+            self._keep += [_i32(inst.act), None]
+        else:
+            self._keep += [None, _i32(inst.pi0)]
+        src, dst, act, pi0 = self._keep
+        st = _Stats()
+        self.h = lib().oracle_open(int(self.bcrp), inst.n, src.size,
+                                   inst.num_actions if self.bcrp else 0, _ptr(src),
+                                   _ptr(act) if act is not None else None, _ptr(dst),
+                                   _ptr(pi0) if pi0 is not None else None, threads,
+                                   ctypes.byref(st))
+        if not self.h:
+            raise MemoryError("oracle_open failed")
+        self.t_pre_s, self.t_label_s = st.t_pre_s, st.t_label_s
+        self.initial_blocks = int(st.initial_blocks)
+
+    def set_state(self, block: np.ndarray, unstable: np.ndarray):
+        b = _i32(block)
+        u = np.ascontiguousarray(unstable, dtype=np.uint8)
+        lib().oracle_set_state(self.h, _ptr(b), u.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)))
+
+    def rounds(self, k: int) -> tuple[int, float]:
+        sec = ctypes.c_double(0.0)
+        done = lib().oracle_rounds(self.h, int(k), self.threads, ctypes.byref(sec))
+        return int(done), sec.value
+
+    def block(self) -> np.ndarray:
+        return np.ctypeslib.as_array(lib().oracle_block(self.h), shape=(self.n,)).copy()
+
+    def close(self):
+        if self.h:
+            lib().oracle_close(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+
+def fast_states(inst, stops, threads: int = 1):
+    """(blocks[k, n], unstable[k, n]) of the reference program after each
+    round in `stops` (ascending), from the event-driven oracle."""
+    stops = np.ascontiguousarray(sorted(int(x) for x in stops), dtype=np.int64)
+    k, n = stops.size, inst.n
+    blocks = np.empty((k, n), np.int32)
+    unstable = np.empty((k, n), np.uint8)
+    bcrp = inst.kind == "bcrp"
+    src, dst = _i32(inst.src), _i32(inst.dst)
+    act = _i32(inst.act) if bcrp else None
+    pi0 = None if bcrp else _i32(inst.pi0)
+    rc = lib().oracle_fast_states(int(bcrp), n, src.size, inst.num_actions if bcrp else 0,
+                                  _ptr(src), _ptr(act) if act is not None else None, _ptr(dst),
+                                  _ptr(pi0) if pi0 is not None else None, k,
+                                  stops.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                  _ptr(blocks),
+                                  unstable.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)),
+                                  threads)
+    if rc != OR_OK:
+        raise RuntimeError(f"oracle_fast_states failed ({rc})")
+    return blocks, unstable

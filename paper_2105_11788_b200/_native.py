@@ -13,13 +13,17 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# BISIM_LIB: developer override (an experimental build of the same library)
-LIB_PATH = os.environ.get("BISIM_LIB") or os.path.join(_HERE, "libbisim.so")
+# BISIM_LIB (developer override: an experimental build of the same library)
+# is honoured only together with BISIM_DEV=1
+LIB_PATH = ((os.environ.get("BISIM_DEV") and os.environ.get("BISIM_LIB"))
+            or os.path.join(_HERE, "libbisim.so"))
 
 BISIM_OK, BISIM_BAD_INPUT, BISIM_GUARD, BISIM_CUDA, BISIM_ABORTED = 0, 1, 2, 3, 4
 SHARD_VERIFY = 1
 DEFAULT_GUARD = -(2 ** 63)
 MODE_AUTO, MODE_PERSISTENT, MODE_STEPPED, MODE_DENSE = 0, 1, 2, 3
+# schedule variants (bisim.h BISIM_FLAG_*): none changes a result
+FLAG_NO_SKIP, FLAG_NO_SOLO, FLAG_CTA_MAJOR, FLAG_LITERAL_LABEL_ROUNDS = 1, 2, 4, 8
 
 i32p = ctypes.POINTER(ctypes.c_int32)
 OBSERVER = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_int64, i32p, ctypes.c_int32, ctypes.c_void_p)
@@ -50,7 +54,9 @@ class Options(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32),
                 ("mode", ctypes.c_int32),
                 ("observer", OBSERVER),
-                ("observer_user", ctypes.c_void_p)]
+                ("observer_user", ctypes.c_void_p),
+                ("flags", ctypes.c_uint32),
+                ("reserved", ctypes.c_int32)]
 
 
 class AutInfo(ctypes.Structure):
@@ -76,7 +82,7 @@ EXPORTS = ("bisim_bcrp", "bisim_rcpp", "bisim_bcrp_ex", "bisim_rcpp_ex", "bisim_
            "bisim_device_count", "bisim_stream", "bisim_version", "bisim_quotient",
            "bisim_is_stable", "bisim_canonical", "bisim_aut_parse", "bisim_aut_read_file",
            "bisim_aut_columns", "bisim_aut_label", "bisim_aut_free", "bisim_bcrp_sharded",
-           "bisim_rcpp_sharded", "bisim_is_stable_under")
+           "bisim_rcpp_sharded", "bisim_is_stable_under", "bisim_preprocess_sorted")
 
 
 def lib():
@@ -107,6 +113,9 @@ def lib():
                                             P(Stats), P(Options)]
             L.bisim_preprocess.argtypes = [i32, i64, i32, i32p, i32p, i32p, i32p, i32p, P(i64),
                                            ctypes.c_int]
+            L.bisim_preprocess_sorted.argtypes = [i32, i64, i32, i32p, i32p, i32p, i32p, i32p, i32p,
+                                                  i32p, i32p, i32p, i32p, i32p, P(i64),
+                                                  ctypes.c_int]
             L.bisim_label_partition.argtypes = [i32, i64, i32, i32p, i32p, i32p, ctypes.c_int]
             L.bisim_quotient.argtypes = [i32, i64, i32, i32p, i32p, i32p, i32p, i32, P(i32),
                                          P(i64), i32p, i32p, i32p, P(i32), ctypes.c_int]
@@ -124,16 +133,18 @@ def lib():
             L.bisim_aut_read_file.argtypes = [ctypes.c_char_p, i32, P(vp), P(AutInfo)]
             L.bisim_aut_columns.argtypes = [vp, i32p, i32p, i32p]
             L.bisim_aut_label.argtypes = [vp, i32, P(i64)]
-            L.bisim_aut_label.restype = vp
             L.bisim_aut_free.argtypes = [vp]
-            L.bisim_aut_free.restype = None
             for name in ("bisim_bcrp", "bisim_rcpp", "bisim_bcrp_ex", "bisim_rcpp_ex",
                          "bisim_bcrp_device", "bisim_rcpp_device", "bisim_preprocess",
                          "bisim_label_partition", "bisim_device_count", "bisim_quotient",
-                         "bisim_is_stable", "bisim_canonical", "bisim_aut_parse", "bisim_aut_read_file",
-           "bisim_aut_columns", "bisim_aut_label", "bisim_aut_free", "bisim_bcrp_sharded",
-           "bisim_rcpp_sharded", "bisim_is_stable_under"):
+                         "bisim_is_stable", "bisim_canonical", "bisim_aut_parse",
+                         "bisim_aut_read_file", "bisim_aut_columns", "bisim_bcrp_sharded",
+                         "bisim_rcpp_sharded", "bisim_is_stable_under", "bisim_preprocess_sorted"):
                 getattr(L, name).restype = ctypes.c_int
+            # pointer / void results: never through the int loop above (a
+            # c_int restype truncates a heap pointer to 32 bits)
+            L.bisim_aut_label.restype = vp
+            L.bisim_aut_free.restype = None
             L.bisim_last_error.restype = ctypes.c_char_p
             L.bisim_last_error.argtypes = []
             L.bisim_stream.restype = ctypes.c_void_p

@@ -67,10 +67,11 @@ class _ObserverBridge:
         self.cfunc = N.OBSERVER(cb)
 
 
-def _options(device: int, mode: int, bridge) -> N.Options:
+def _options(device: int, mode: int, bridge, flags: int = 0) -> N.Options:
     o = N.Options()
     o.device = device
     o.mode = mode
+    o.flags = flags
     if bridge is not None:
         o.observer = bridge.cfunc
     return o
@@ -90,11 +91,12 @@ def _raise_for(rc: int, bridge, guard_msg_stats: N.Stats):
 
 
 def bcrp_arrays(n: int, src, act, dst, num_actions: int, *, max_supersteps: int | None = None,
-                observer=None, device: int = 0, mode: int = N.MODE_AUTO):
+                observer=None, device: int = 0, mode: int = N.MODE_AUTO, flags: int = 0):
     """Coarsest bisimulation of the LTS given by int32 columns.
 
     Returns ``(block, RunStats, native_stats)`` where ``block`` is an int32
-    numpy array in canonical leader form.
+    numpy array in canonical leader form.  ``flags`` (``_native.FLAG_*``)
+    selects another schedule of the same program; results never change.
     """
     src, act, dst = N.as_i32(src), N.as_i32(act), N.as_i32(dst)
     m = src.size
@@ -104,7 +106,7 @@ def bcrp_arrays(n: int, src, act, dst, num_actions: int, *, max_supersteps: int 
     splits = np.zeros(cap, np.int32)
     st = N.Stats()
     bridge = _ObserverBridge(observer) if observer is not None else None
-    opt = _options(device, mode, bridge)  # an observer implies stepped rounds
+    opt = _options(device, mode, bridge, flags)  # an observer implies stepped rounds
     rc = N.lib().bisim_bcrp_ex(n, m, int(num_actions), N.ptr(src), N.ptr(act), N.ptr(dst), guard,
                                N.ptr(block), N.ptr(splits), cap, ctypes.byref(st),
                                ctypes.byref(opt))
@@ -157,34 +159,30 @@ def partition_by_outgoing_labels(lts, policy, *, common_election: bool | None = 
 
 
 def preprocess(lts, device: int = 0) -> BcrpAux:
-    """Label-ordering tables (bcrp.py:116-126).
-
-    order/nr_marks/off/mark_length come from the GPU preprocessing kernels
-    (label masks + slot ranks).  The refinement path never sorts transitions;
-    only this table export arranges them in the reference's stable
-    (source, action) order.
+    """Label-ordering tables (bcrp.py:116-126), computed on the GPU
+    (``bisim_preprocess_sorted``): the transitions stably sorted by (source,
+    action) with a device radix sort, then action_switch, order, nr_marks,
+    off and mark_length of that order.  The refinement path itself never
+    sorts; this is the reference's table export.
     """
     n, src, act, dst, A = lts_columns(lts)
     m = src.size
-    order = np.empty(max(m, 1), np.int32)
+    mm = max(m, 1)
+    perm, s_src, s_act, s_dst, sw, order = (np.empty(mm, np.int32) for _ in range(6))
     nr = np.empty(n, np.int32)
     off = np.empty(n, np.int32)
     L = ctypes.c_int64(0)
-    rc = N.lib().bisim_preprocess(n, m, A, N.ptr(src), N.ptr(act), N.ptr(order), N.ptr(nr),
-                                  N.ptr(off), ctypes.byref(L), device)
+    rc = N.lib().bisim_preprocess_sorted(n, m, A, N.ptr(src), N.ptr(act), N.ptr(dst), N.ptr(perm),
+                                         N.ptr(s_src), N.ptr(s_act), N.ptr(s_dst), N.ptr(sw),
+                                         N.ptr(order), N.ptr(nr), N.ptr(off), ctypes.byref(L),
+                                         device)
     if rc == N.BISIM_BAD_INPUT:
         raise ValueError(N.last_error())
     N.check(rc)
-    perm = np.lexsort((act, src)) if m else np.zeros(0, np.int64)  # stable (source, action)
-    s_src, s_act, s_dst = src[perm], act[perm], dst[perm]
-    switch = np.zeros(m, np.int32)
-    if m > 1:
-        switch[1:] = ((s_src[1:] == s_src[:-1]) & (s_act[1:] != s_act[:-1])).astype(np.int32)
-    labels = lts.action_labels
-    sorted_lts = Lts.from_arrays(n, s_src, s_act, s_dst, labels,
+    sorted_lts = Lts.from_arrays(n, s_src[:m], s_act[:m], s_dst[:m], lts.action_labels,
                                  getattr(lts, "initial_state", 0), validate=False)
-    return BcrpAux(lts=sorted_lts, action_switch=tuple(switch.tolist()),
-                   order=tuple(order[:m][perm].tolist()), nr_marks=tuple(nr.tolist()),
+    return BcrpAux(lts=sorted_lts, action_switch=tuple(sw[:m].tolist()),
+                   order=tuple(order[:m].tolist()), nr_marks=tuple(nr.tolist()),
                    off=tuple(off.tolist()), mark_length=int(L.value))
 
 

@@ -23,6 +23,8 @@
 #include "kernels_sparse.cuh"
 #include "kernels_label.cuh"
 
+#include <cub/device/device_radix_sort.cuh>
+
 namespace bisim {
 namespace {
 
@@ -70,7 +72,7 @@ struct Ctx {
     DevBuf src, act, dst, pi0, lmask, off, rev_ptr, cursor, rev_slot, block, nl, mark, unstable,
         split_list, cmem, splits, ctrl, scan_tmp, rev2, members, bstart, bsize, tblock,
         small_list, big_list, big_base, tmp, scnt, smin, kcur, scur, counter, brange, bar, trace, lhash, lkeys,
-        lmins, sarr, big_list4, big_base4, big_info, big_info4, sinfo;
+        lmins, sarr, big_list4, big_base4, big_info, big_info4, sinfo, nrm;
     int launches = 0;
 };
 
@@ -204,6 +206,129 @@ int64_t loop_bytes(bool bcrp, bool dense, int32_t n, int64_t L, int64_t R, const
     return (R + 1) * 64 + (int64_t)ls.work_edges * per_edge + (int64_t)ls.work_members * per_member;
 }
 
+// Developer tuning knobs (kernel-variant sweeps, tracing): read only when
+// BISIM_DEV=1, so a production call never depends on the environment.
+const char* dev_env(const char* name) { return getenv("BISIM_DEV") ? getenv(name) : nullptr; }
+
+// Label pre-partition (bcrp.py:144-184) into block[]: canonical grouping by
+// a verified 64-bit hash of each state's label set (kernels_label.cuh); a
+// hash collision -- or `literal` -- runs the literal |Act| mark-and-split
+// rounds in one cooperative kernel instead.  Both give the same canonical
+// pi0 (states grouped by outgoing label set, min-id leaders).
+void label_partition_dev(Ctx& c, int32_t n, int32_t A, const unsigned long long* lmask, int32_t* block,
+                         bool literal) {
+    cudaStream_t st = c.stream;
+    const int32_t W = (A + 63) / 64;
+    const int TB = 256;
+    CK(cudaMemsetAsync(block, 0, (int64_t)n * 4, st));
+    if (A == 0) return;
+    if (!literal) {
+        uint64_t T = 1024;
+        while (T < 2ull * (uint64_t)n) T <<= 1;
+        auto* h = (unsigned long long*)c.lhash.ensure((int64_t)n * 8);
+        auto* keys = (unsigned long long*)c.lkeys.ensure(T * 8);
+        auto* mins = (int32_t*)c.lmins.ensure(T * 4 + 4);
+        int32_t* mismatch = mins + T;
+        CK(cudaMemsetAsync(keys, 0, T * 8, st));
+        CK(cudaMemsetAsync(mins, 0x7f, T * 4 + 4, st));
+        CK(cudaMemsetAsync(mismatch, 0, 4, st));
+        k_label_hash<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, W, lmask, h);
+        k_label_insert<<<c.sms * 2, 512, 0, st>>>(n, h, keys, mins, T - 1);
+        k_label_assign<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, W, h, keys, mins, T - 1, lmask, block,
+                                                              mismatch);
+        c.launches += 3;
+        int32_t hm = 0;
+        CK(cudaMemcpyAsync(&hm, mismatch, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        literal = hm != 0;
+        if (literal) CK(cudaMemsetAsync(block, 0, (int64_t)n * 4, st));
+    }
+    if (literal) {
+        unsigned long long* nl = (unsigned long long*)c.nl.ensure((int64_t)n * 8);
+        CK(cudaMemsetAsync(nl, 0, (int64_t)n * 8, st));
+        int32_t nn = n, AA = A;
+        const unsigned long long* lm = lmask;
+        void* args[] = {&nn, &AA, (void*)&lm, &block, &nl};
+        CK(cudaLaunchCooperativeKernel((const void*)k_label_rounds, c.grid_label, kThreads, args, 0, st));
+        ++c.launches;
+    }
+}
+
+// Error mapping for the table entry points (same codes as the loop calls).
+template <typename F>
+int guarded_call(F&& f) {
+    try {
+        g_last_error.clear();
+        f();
+        return BISIM_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return BISIM_CUDA;
+    }
+}
+
+// Device label tables of a host transition list: inputs copied, validated
+// (read back BEFORE anything indexes by them), label masks, nr_marks and
+// off = exclusive scan (bcrp.py:91-113).
+struct LabelTables {
+    const int32_t *src = nullptr, *act = nullptr, *dst = nullptr;
+    unsigned long long* lmask = nullptr;
+    int32_t* nr = nullptr;   // nr_marks[n]
+    int32_t* off = nullptr;  // off[n+1]
+    int64_t L = 0;
+};
+
+LabelTables label_tables(Ctx& c, int32_t n, int64_t m, int32_t A, const int32_t* src, const int32_t* act,
+                         const int32_t* dst = nullptr) {
+    if (n < 1) throw Error(BISIM_BAD_INPUT, "state count must be at least 1");
+    if (m < 0 || m >= (int64_t)INT32_MAX) throw Error(BISIM_BAD_INPUT, "transition count out of range");
+    if (A < 0) throw Error(BISIM_BAD_INPUT, "negative action count");
+    if (n >= (1 << 30)) throw Error(BISIM_BAD_INPUT, "state count above 2^30 is not supported");
+    if (m > 0 && (!src || !act)) throw Error(BISIM_BAD_INPUT, "null transition array");
+    CK(cudaSetDevice(c.device));
+    c.launches = 0;
+    cudaStream_t st = c.stream;
+    const int TB = 256;
+    const int64_t mm = std::max<int64_t>(m, 1);
+    const int32_t W = std::max((A + 63) / 64, 1);
+    LabelTables t;
+    int32_t* d_src = (int32_t*)c.src.ensure(mm * 4);
+    int32_t* d_act = (int32_t*)c.act.ensure(mm * 4);
+    int32_t* d_dst = dst ? (int32_t*)c.dst.ensure(mm * 4) : d_src;
+    if (m) {
+        CK(cudaMemcpyAsync(d_src, src, m * 4, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d_act, act, m * 4, cudaMemcpyHostToDevice, st));
+        if (dst) CK(cudaMemcpyAsync(d_dst, dst, m * 4, cudaMemcpyHostToDevice, st));
+    }
+    Ctrl* ctrl = (Ctrl*)c.ctrl.ensure(std::max(sizeof(Ctrl), sizeof(SCtrl)));
+    t.lmask = (unsigned long long*)c.lmask.ensure((size_t)W * n * 8);
+    CK(cudaMemsetAsync(ctrl, 0, sizeof(Ctrl), st));
+    CK(cudaMemsetAsync(t.lmask, 0, (size_t)W * n * 8, st));
+    // k_label_mask checks src/act/dst ranges (dst := src when not given)
+    if (m) k_label_mask<<<grid_for(m, TB, c.sms), TB, 0, st>>>(n, m, A, d_src, d_act, d_dst, t.lmask, ctrl);
+    int32_t bad = 0;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(&bad, &ctrl->bad, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (bad) throw Error(BISIM_BAD_INPUT, "transition mentions a state or action outside range");
+    t.nr = (int32_t*)c.nrm.ensure((int64_t)n * 4);
+    t.off = (int32_t*)c.off.ensure(((int64_t)n + 1) * 4);
+    k_nr_marks<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, W, t.lmask, t.off);
+    CK(cudaMemcpyAsync(t.nr, t.off, (int64_t)n * 4, cudaMemcpyDeviceToDevice, st));
+    scan_excl(c, t.off, n);
+    int32_t L32 = 0;
+    CK(cudaMemcpyAsync(&L32, t.off + n, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    t.L = L32;
+    t.src = d_src;
+    t.act = d_act;
+    t.dst = dst ? d_dst : nullptr;
+    return t;
+}
+
 int run_with(Ctx& c, Job& j);
 
 int run(Job& j) { return run_with(*get_ctx(j.opt.device), j); }
@@ -304,6 +429,17 @@ int run_with(Ctx& c, Job& j) {
         k_check_pi0<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, d_pi0, ctrl);
         ++c.launches;
     }
+    // Validation must finish before anything scatters through src/dst
+    // (k_indeg, the reverse fill): read the flag back here.
+    {
+        int32_t bad = 0;
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(&bad, &ctrl->bad, sizeof(bad), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (bad)
+            throw Error(BISIM_BAD_INPUT, j.bcrp ? "transition mentions a state or action outside range"
+                                                : "edge outside 0..n-1 or pi0 is not a leader-form partition");
+    }
     CK(cudaMemsetAsync(rev_ptr, 0, ((int64_t)n + 1) * 4, st));
     if (m) {
         k_indeg<<<grid_for(m, TB, c.sms), TB, 0, st>>>(m, d_dst, rev_ptr, sharded ? d_src : nullptr, src_lo,
@@ -340,15 +476,10 @@ int run_with(Ctx& c, Job& j) {
         ++c.launches;
     }
     CK(cudaGetLastError());
-    Ctrl hc;
-    CK(cudaMemcpyAsync(&hc, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
     int32_t L32 = n;
     if (j.bcrp) CK(cudaMemcpyAsync(&L32, off + n, 4, cudaMemcpyDeviceToHost, st));
     CK(cudaEventRecord(c.ev[2], st));
     CK(cudaStreamSynchronize(st));
-    if (hc.bad)
-        throw Error(BISIM_BAD_INPUT, j.bcrp ? "transition mentions a state or action outside range"
-                                            : "edge outside 0..n-1 or pi0 is not a leader-form partition");
     S.mark_length = L32;
 
     // ---- label pre-partition (bcrp.py:144-184) / pi0 (rcpp.py:58-72)
@@ -359,38 +490,7 @@ int run_with(Ctx& c, Job& j) {
     }
     unsigned long long* nl = (unsigned long long*)c.nl.ensure((int64_t)n * 8);
     if (j.bcrp) {
-        CK(cudaMemsetAsync(block, 0, (int64_t)n * 4, st));
-        bool literal = A > 0 && getenv("BISIM_LITERAL_LABEL_ROUNDS") != nullptr;
-        if (A > 0 && !literal) {
-            // canonical grouping by label set (kernels_label.cuh), verified
-            uint64_t T = 1024;
-            while (T < 2ull * (uint64_t)n) T <<= 1;
-            auto* h = (unsigned long long*)c.lhash.ensure((int64_t)n * 8);
-            auto* keys = (unsigned long long*)c.lkeys.ensure(T * 8);
-            auto* mins = (int32_t*)c.lmins.ensure(T * 4 + 4);
-            int32_t* mismatch = mins + T;
-            CK(cudaMemsetAsync(keys, 0, T * 8, st));
-            CK(cudaMemsetAsync(mins, 0x7f, T * 4 + 4, st));
-            CK(cudaMemsetAsync(mismatch, 0, 4, st));
-            k_label_hash<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, W, lmask, h);
-            k_label_insert<<<c.sms * 2, 512, 0, st>>>(n, h, keys, mins, T - 1);
-            k_label_assign<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, W, h, keys, mins, T - 1, lmask, block,
-                                                                  mismatch);
-            c.launches += 3;
-            int32_t hm = 0;
-            CK(cudaMemcpyAsync(&hm, mismatch, 4, cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-            literal = hm != 0;  // a 64-bit hash collision: redo with the literal rounds
-            if (literal) CK(cudaMemsetAsync(block, 0, (int64_t)n * 4, st));
-        }
-        if (literal) {
-            CK(cudaMemsetAsync(nl, 0, (int64_t)n * 8, st));
-            int32_t nn = n, AA = A;
-            const unsigned long long* lm = lmask;
-            void* args[] = {&nn, &AA, (void*)&lm, &block, &nl};
-            CK(cudaLaunchCooperativeKernel((const void*)k_label_rounds, c.grid_label, kThreads, args, 0, st));
-            ++c.launches;
-        }
+        label_partition_dev(c, n, A, lmask, block, (j.opt.flags & BISIM_FLAG_LITERAL_LABEL_ROUNDS) != 0);
     } else {
         CK(cudaMemcpyAsync(block, d_pi0, (int64_t)n * 4, cudaMemcpyDeviceToDevice, st));
     }
@@ -495,22 +595,21 @@ int run_with(Ctx& c, Job& j) {
         sp.splits = splits;
         sp.ctrl = (SCtrl*)ctrl;
         sp.bar = (GridBarrier*)c.bar.ensure(sizeof(GridBarrier));
-        // BISIM_NO_SKIP=1 disables no-op-round retirement (every round runs)
-        sp.allow_skip = getenv("BISIM_NO_SKIP") == nullptr ? 1 : 0;
-        sp.cta_minor = getenv("BISIM_CTA_MAJOR") == nullptr ? 1 : 0;
-        // BISIM_NO_SOLO=1 keeps every round on the whole grid
-        sp.allow_solo = getenv("BISIM_NO_SOLO") == nullptr ? 1 : 0;
+        // schedule variants (bisim.h BISIM_FLAG_*); none changes a result
+        sp.allow_skip = (j.opt.flags & BISIM_FLAG_NO_SKIP) ? 0 : 1;
+        sp.cta_minor = (j.opt.flags & BISIM_FLAG_CTA_MAJOR) ? 0 : 1;
+        sp.allow_solo = (j.opt.flags & BISIM_FLAG_NO_SOLO) ? 0 : 1;
         // developer: BISIM_MODE_B=1|2 forces the wide / two-pass phase-B layout
-        sp.force_mode_b = getenv("BISIM_MODE_B") ? atoi(getenv("BISIM_MODE_B")) : -1;
-        sp.batch_min_c = getenv("BISIM_BATCH_C") ? atoi(getenv("BISIM_BATCH_C")) : 8192;
-        sp.onepass_major = getenv("BISIM_ONEPASS_MINOR") != nullptr ? 0
-                           : getenv("BISIM_MAJOR") ? atoi(getenv("BISIM_MAJOR")) : kSparseThreads / 32;
-        sp.wide_major = getenv("BISIM_WIDE_MAJOR") ? atoi(getenv("BISIM_WIDE_MAJOR")) : 0;
-        sp.prefetch_next = getenv("BISIM_PREFETCH") ? atoi(getenv("BISIM_PREFETCH")) : 1;
-        sp.solo_max_c = getenv("BISIM_SOLO_C") ? atoi(getenv("BISIM_SOLO_C")) : kSoloMaxC;
-        sp.solo_max_items = getenv("BISIM_SOLO_ITEMS") ? atoi(getenv("BISIM_SOLO_ITEMS")) : kSoloMaxItems;
+        sp.force_mode_b = dev_env("BISIM_MODE_B") ? atoi(dev_env("BISIM_MODE_B")) : -1;
+        sp.batch_min_c = dev_env("BISIM_BATCH_C") ? atoi(dev_env("BISIM_BATCH_C")) : 8192;
+        sp.onepass_major = dev_env("BISIM_ONEPASS_MINOR") != nullptr ? 0
+                           : dev_env("BISIM_MAJOR") ? atoi(dev_env("BISIM_MAJOR")) : kSparseThreads / 32;
+        sp.wide_major = dev_env("BISIM_WIDE_MAJOR") ? atoi(dev_env("BISIM_WIDE_MAJOR")) : 0;
+        sp.prefetch_next = dev_env("BISIM_PREFETCH") ? atoi(dev_env("BISIM_PREFETCH")) : 1;
+        sp.solo_max_c = dev_env("BISIM_SOLO_C") ? atoi(dev_env("BISIM_SOLO_C")) : kSoloMaxC;
+        sp.solo_max_items = dev_env("BISIM_SOLO_ITEMS") ? atoi(dev_env("BISIM_SOLO_ITEMS")) : kSoloMaxItems;
         // developer tracing: BISIM_TRACE=<rounds> BISIM_TRACE_FILE=<path>
-        if (const char* tr = getenv("BISIM_TRACE")) {
+        if (const char* tr = dev_env("BISIM_TRACE")) {
             sp.trace_rounds = atoll(tr);
             sp.trace = (unsigned long long*)c.trace.ensure(sp.trace_rounds * 8 * kTraceWords + 64);
             CK(cudaMemsetAsync(sp.trace, 0, sp.trace_rounds * 8 * kTraceWords, st));
@@ -640,7 +739,7 @@ int run_with(Ctx& c, Job& j) {
     if (!dense && sp.trace) {
         std::vector<unsigned long long> t(sp.trace_rounds * kTraceWords);
         CK(cudaMemcpy(t.data(), sp.trace, t.size() * 8, cudaMemcpyDeviceToHost));
-        const char* path = getenv("BISIM_TRACE_FILE");
+        const char* path = dev_env("BISIM_TRACE_FILE");
         if (FILE* f = fopen(path ? path : "bisim_trace.csv", "w")) {
             fprintf(f, "round,phaseA_ns,barrierA_ns,phaseB_ns,csize,solo,n_small,big_chunks,n_big,"
                        "b_tag_ns,b_sync1_ns,b_arrive_ns,b_sync2_ns,b_place_ns,mode_b\n");
@@ -713,6 +812,14 @@ std::vector<int32_t> shard_bounds(Ctx& c, int32_t n, int64_t m, const int32_t* d
         for (int g = 1; g < G; ++g) lo[g] = (int32_t)((int64_t)n * g / G);
         return lo;
     }
+    // validate src before scattering through it (the replicas check the rest)
+    Ctrl* ctrl = (Ctrl*)c.ctrl.ensure(std::max(sizeof(Ctrl), sizeof(SCtrl)));
+    CK(cudaMemsetAsync(ctrl, 0, sizeof(Ctrl), c.stream));
+    k_check_edges<<<grid_for(m, 256, c.sms), 256, 0, c.stream>>>(n, m, d_src, d_src, ctrl);
+    int32_t bad = 0;
+    CK(cudaMemcpyAsync(&bad, &ctrl->bad, sizeof(bad), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    if (bad) throw Error(BISIM_BAD_INPUT, "transition mentions a state outside range");
     int32_t* deg = (int32_t*)c.cursor.ensure(((int64_t)n + 1) * 4);
     CK(cudaMemsetAsync(deg, 0, ((int64_t)n + 1) * 4, c.stream));
     k_indeg<<<grid_for(m, 256, c.sms), 256, 0, c.stream>>>(m, d_src, deg);
@@ -1064,91 +1171,91 @@ int bisim_rcpp_sharded(int32_t n, int64_t m, const int32_t* src, const int32_t* 
 int bisim_preprocess(int32_t n, int64_t m, int32_t num_actions, const int32_t* src, const int32_t* act,
                      int32_t* order_out, int32_t* nr_marks_out, int32_t* off_out, int64_t* mark_length,
                      int device) {
-    try {
-        g_last_error.clear();
-        if (n < 1 || m < 0 || m >= (int64_t)INT32_MAX || num_actions < 0)
-            throw Error(BISIM_BAD_INPUT, "bad sizes");
+    return guarded_call([&]() {
         Ctx& c = *get_ctx(device);
         std::lock_guard<std::mutex> lock(c.mu);
-        CK(cudaSetDevice(c.device));
+        LabelTables t = label_tables(c, n, m, num_actions, src, act);
         cudaStream_t st = c.stream;
-        const int64_t mm = std::max<int64_t>(m, 1);
-        const int32_t W = (num_actions + 63) / 64;
-        int32_t* d_src = (int32_t*)c.src.ensure(mm * 4);
-        int32_t* d_act = (int32_t*)c.act.ensure(mm * 4);
-        int32_t* d_order = (int32_t*)c.rev_slot.ensure(mm * 4);
-        Ctrl* ctrl = (Ctrl*)c.ctrl.ensure(sizeof(Ctrl));
-        auto* lmask = (unsigned long long*)c.lmask.ensure((size_t)std::max(W, 1) * n * 8);
-        int32_t* off = (int32_t*)c.off.ensure(((int64_t)n + 1) * 4);
-        if (m) {
-            CK(cudaMemcpyAsync(d_src, src, m * 4, cudaMemcpyHostToDevice, st));
-            CK(cudaMemcpyAsync(d_act, act, m * 4, cudaMemcpyHostToDevice, st));
-        }
-        CK(cudaMemsetAsync(ctrl, 0, sizeof(Ctrl), st));
-        CK(cudaMemsetAsync(lmask, 0, (size_t)std::max(W, 1) * n * 8, st));
         const int TB = 256;
-        if (m) k_label_mask<<<grid_for(m, TB, c.sms), TB, 0, st>>>(n, m, num_actions, d_src, d_act, d_src, lmask, ctrl);
-        k_nr_marks<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, W, lmask, off);
-        if (nr_marks_out) CK(cudaMemcpyAsync(nr_marks_out, off, (int64_t)n * 4, cudaMemcpyDeviceToHost, st));
-        scan_excl(c, off, n);
-        if (m) k_order<<<grid_for(m, TB, c.sms), TB, 0, st>>>(n, m, d_src, d_act, lmask, d_order);
+        int32_t* d_order = (int32_t*)c.rev_slot.ensure(std::max<int64_t>(m, 1) * 4);
+        if (m) k_order<<<grid_for(m, TB, c.sms), TB, 0, st>>>(n, m, t.src, t.act, t.lmask, d_order);
         CK(cudaGetLastError());
-        Ctrl hc;
-        int32_t L32 = 0;
-        CK(cudaMemcpyAsync(&hc, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(&L32, off + n, 4, cudaMemcpyDeviceToHost, st));
-        if (off_out) CK(cudaMemcpyAsync(off_out, off, (int64_t)n * 4, cudaMemcpyDeviceToHost, st));
+        if (nr_marks_out) CK(cudaMemcpyAsync(nr_marks_out, t.nr, (int64_t)n * 4, cudaMemcpyDeviceToHost, st));
+        if (off_out) CK(cudaMemcpyAsync(off_out, t.off, (int64_t)n * 4, cudaMemcpyDeviceToHost, st));
         if (order_out && m) CK(cudaMemcpyAsync(order_out, d_order, m * 4, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        if (hc.bad) throw Error(BISIM_BAD_INPUT, "transition mentions a state or action outside range");
-        if (mark_length) *mark_length = L32;
-        return BISIM_OK;
-    } catch (const Error& e) {
-        g_last_error = e.what();
-        return e.code;
-    } catch (const std::exception& e) {
-        g_last_error = e.what();
-        return BISIM_CUDA;
-    }
+        if (mark_length) *mark_length = t.L;
+    });
+}
+
+int bisim_preprocess_sorted(int32_t n, int64_t m, int32_t num_actions, const int32_t* src, const int32_t* act,
+                            const int32_t* dst, int32_t* perm_out, int32_t* src_out, int32_t* act_out,
+                            int32_t* dst_out, int32_t* action_switch_out, int32_t* order_out,
+                            int32_t* nr_marks_out, int32_t* off_out, int64_t* mark_length, int device) {
+    return guarded_call([&]() {
+        if (m > 0 && !dst && dst_out) throw Error(BISIM_BAD_INPUT, "null dst with dst_out");
+        Ctx& c = *get_ctx(device);
+        std::lock_guard<std::mutex> lock(c.mu);
+        LabelTables t = label_tables(c, n, m, num_actions, src, act, m ? dst : nullptr);
+        cudaStream_t st = c.stream;
+        const int TB = 256;
+        const int64_t mm = std::max<int64_t>(m, 1);
+        // stable sort by (source, action): radix sort of the key
+        // source * |Act| + action carrying the transition index (bcrp.py:49-52)
+        auto* keys = (unsigned long long*)c.lkeys.ensure(mm * 8 * 2);
+        unsigned long long* keys_sorted = keys + mm;
+        int32_t* idx = (int32_t*)c.cursor.ensure(mm * 4 * 2);
+        int32_t* perm = idx + mm;
+        if (m) {
+            k_sort_keys<<<grid_for(m, TB, c.sms), TB, 0, st>>>(m, num_actions, t.src, t.act, keys, idx);
+            const unsigned long long maxkey = (unsigned long long)n * (unsigned long long)std::max(num_actions, 1);
+            int bits = 1;
+            while (bits < 64 && (1ull << bits) < maxkey) ++bits;
+            size_t tmp_bytes = 0;
+            CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys_sorted, idx, perm, (int)m, 0, bits,
+                                               st));
+            void* tmp = c.scan_tmp.ensure(tmp_bytes);
+            CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_sorted, idx, perm, (int)m, 0, bits, st));
+            c.launches += 2;
+        }
+        // per sorted transition: columns, action_switch (bcrp.py:55-65), order
+        int32_t* cols = (int32_t*)c.rev2.ensure(mm * 4 * 5);
+        int32_t *s_src = cols, *s_act = cols + mm, *s_dst = cols + 2 * mm, *s_sw = cols + 3 * mm,
+                *s_ord = cols + 4 * mm;
+        const int32_t* d_dst = t.dst;
+        if (m)
+            k_sorted_tables<<<grid_for(m, TB, c.sms), TB, 0, st>>>(n, m, perm, t.src, t.act, d_dst, t.lmask, s_src,
+                                                                   s_act, s_dst, s_sw, s_ord);
+        CK(cudaGetLastError());
+        auto d2h = [&](int32_t* out, const int32_t* d, int64_t cnt) {
+            if (out && cnt) CK(cudaMemcpyAsync(out, d, cnt * 4, cudaMemcpyDeviceToHost, st));
+        };
+        d2h(perm_out, perm, m);
+        d2h(src_out, s_src, m);
+        d2h(act_out, s_act, m);
+        if (d_dst) d2h(dst_out, s_dst, m);
+        d2h(action_switch_out, s_sw, m);
+        d2h(order_out, s_ord, m);
+        d2h(nr_marks_out, t.nr, n);
+        d2h(off_out, t.off, n);
+        CK(cudaStreamSynchronize(st));
+        if (mark_length) *mark_length = t.L;
+    });
 }
 
 int bisim_label_partition(int32_t n, int64_t m, int32_t num_actions, const int32_t* src, const int32_t* act,
                           int32_t* block_out, int device) {
-    // The label partition is the pi0 of a BCRP run; run a BCRP job with a
-    // guard of exactly |Act| so the main loop never starts, and read pi0.
-    try {
-        g_last_error.clear();
-        std::vector<int32_t> dst(std::max<int64_t>(m, 1), 0);
-        Job j;
-        j.bcrp = true;
-        j.n = n;
-        j.m = m;
-        j.A = num_actions;
-        j.src = src;
-        j.act = act;
-        j.dst = m ? src : nullptr;  // targets are irrelevant for the label rounds
-        j.max_supersteps = num_actions;  // main loop's first superstep trips the guard
-        j.block_out = block_out;
-        j.opt.device = device;
-        bisim_stats S{};
-        j.st = &S;
-        try {
-            run(j);
-        } catch (const Error& e) {
-            if (e.code != BISIM_GUARD || S.guard_count != (int64_t)num_actions + 1) throw;
-        }
-        // block buffer holds pi0: the guard fired before any round ran
+    return guarded_call([&]() {
+        if (!block_out) throw Error(BISIM_BAD_INPUT, "null block_out");
         Ctx& c = *get_ctx(device);
         std::lock_guard<std::mutex> lock(c.mu);
-        CK(cudaMemcpy(block_out, c.block.p, (int64_t)n * 4, cudaMemcpyDeviceToHost));
-        return BISIM_OK;
-    } catch (const Error& e) {
-        g_last_error = e.what();
-        return e.code;
-    } catch (const std::exception& e) {
-        g_last_error = e.what();
-        return BISIM_CUDA;
-    }
+        LabelTables t = label_tables(c, n, m, num_actions, src, act);
+        int32_t* block = (int32_t*)c.block.ensure((int64_t)n * 4);
+        label_partition_dev(c, n, num_actions, t.lmask, block, false);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(block_out, block, (int64_t)n * 4, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaStreamSynchronize(c.stream));
+    });
 }
 
 const char* bisim_last_error(void) { return g_last_error.c_str(); }

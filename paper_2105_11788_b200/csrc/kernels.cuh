@@ -242,6 +242,44 @@ __global__ void k_order(int32_t n, int64_t m, const int32_t* __restrict__ src,
         order[i] = label_rank(lmask, n, src[i], act[i]);
 }
 
+// preprocess() export: radix-sort keys source * |Act| + action with the
+// transition index as payload (a stable sort by (source, action),
+// bcrp.py:49-52).
+__global__ void k_sort_keys(int64_t m, int32_t A, const int32_t* __restrict__ src,
+                            const int32_t* __restrict__ act, unsigned long long* keys, int32_t* idx) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        keys[i] = (unsigned long long)src[i] * (unsigned long long)(A > 0 ? A : 1) + (unsigned)act[i];
+        idx[i] = (int32_t)i;
+    }
+}
+
+// Tables of the sorted transition list (BcrpAux, bcrp.py:116-126): sorted
+// columns, action_switch[k] = same source and a different action than
+// transition k-1 (bcrp.py:55-65), order[k] = rank of the action among the
+// source's labels -- the segmented inclusive scan of action_switch
+// (bcrp.py:68-104) restated as a popcount of lower label bits.
+__global__ void k_sorted_tables(int32_t n, int64_t m, const int32_t* __restrict__ perm,
+                                const int32_t* __restrict__ src, const int32_t* __restrict__ act,
+                                const int32_t* __restrict__ dst, const unsigned long long* __restrict__ lmask,
+                                int32_t* s_src, int32_t* s_act, int32_t* s_dst, int32_t* s_sw, int32_t* s_ord) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t i = perm[k];
+        const int32_t s = src[i], a = act[i];
+        s_src[k] = s;
+        s_act[k] = a;
+        if (dst) s_dst[k] = dst[i];
+        int32_t sw = 0;
+        if (k > 0) {
+            const int32_t p = perm[k - 1];
+            sw = (src[p] == s && act[p] != a) ? 1 : 0;
+        }
+        s_sw[k] = sw;
+        s_ord[k] = label_rank(lmask, n, s, a);
+    }
+}
+
 // in-degree histogram, warp-aggregated on equal targets
 // In-degrees; with src != nullptr only transitions whose source lies in
 // [lo, hi) count (one shard of the transition-sharded mode).

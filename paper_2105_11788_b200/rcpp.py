@@ -72,7 +72,7 @@ def _relation_columns(rel):
 
 
 def rcpp_arrays(n: int, src, dst, pi0, *, max_supersteps: int | None = None, observer=None,
-                device: int = 0, mode: int = N.MODE_AUTO):
+                device: int = 0, mode: int = N.MODE_AUTO, flags: int = 0):
     """Refine leader-form ``pi0`` over edges (src[i], dst[i]).
 
     Returns ``(block, RunStats, native_stats)``.
@@ -86,7 +86,7 @@ def rcpp_arrays(n: int, src, dst, pi0, *, max_supersteps: int | None = None, obs
     splits = np.zeros(cap, np.int32)
     st = N.Stats()
     bridge = _ObserverBridge(observer) if observer is not None else None
-    opt = _options(device, mode, bridge)  # an observer implies stepped rounds
+    opt = _options(device, mode, bridge, flags)  # an observer implies stepped rounds
     rc = N.lib().bisim_rcpp_ex(n, src.size, N.ptr(src), N.ptr(dst), N.ptr(pi0), guard,
                                N.ptr(block), N.ptr(splits), cap, ctypes.byref(st),
                                ctypes.byref(opt))

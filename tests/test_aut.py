@@ -130,3 +130,32 @@ def test_read_aut_file(tmp_path):
     with pytest.raises(ParseError):
         (tmp_path / "e.aut").write_text("", encoding="utf-8")
         read_aut(tmp_path / "e.aut")
+
+
+def test_long_labels_parse_from_worker_thread(tmp_path):
+    """Labels longer than the std::string inline buffer live on the heap of
+    the calling thread's malloc arena (mmapped high addresses off the main
+    thread): the label pointer must come back untruncated."""
+    import threading
+    labels = ["a_rather_long_action_label_%03d" % i for i in range(40)]
+    lines = ["des (0, %d, 50)" % len(labels)]
+    lines += ['(%d, "%s", %d)' % (i, labels[i], (i * 7 + 3) % 50) for i in range(len(labels))]
+    text = "\n".join(lines) + "\n"
+    path = tmp_path / "long.aut"
+    path.write_text(text)
+    out = {}
+
+    def work():
+        try:
+            out["parse"] = parse_aut(text, threads=2)
+            out["read"] = read_aut(path, threads=2)
+        except BaseException as e:  # noqa: BLE001
+            out["exc"] = e
+
+    t = threading.Thread(target=work)
+    t.start()
+    t.join()
+    assert "exc" not in out, out.get("exc")
+    for lts in (out["parse"], out["read"]):
+        assert list(lts.action_labels) == sorted(labels)
+        assert lts.n == 50

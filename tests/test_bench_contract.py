@@ -1,34 +1,40 @@
-"""bench.py contract: the round counts the CPU reference arm extrapolates
-with (bench.KNOWN_SUPERSTEPS) are the ones the GPU path produces, and the
-bench instances are the documented configs."""
-import numpy as np
-import pytest
+"""bench.py contract (CPU): both arms print the same config for a workload,
+the round counts they use come from CPU-oracle runs to completion (not from
+the GPU), and the reference arm runs end to end on a small config."""
+import json
+import os
+import subprocess
+import sys
 
 import bench
-from paper_2105_11788_b200 import bcrp_arrays, rcpp_arrays
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def test_known_supersteps_cover_all_configs():
-    assert set(bench.KNOWN_SUPERSTEPS) == {"c1", "c2", "c3", "c4u", "c4l", "c5"}
-    assert bench.KNOWN_SUPERSTEPS["c3"] == 2 * 200_000 - 2      # chain: 2n-2 (analytic)
+def test_oracle_runstats_cover_all_configs():
+    for c in ("c1", "c2", "c3", "c4u", "c4l", "c5", "c5s"):
+        rec = bench.oracle_runstats(c)
+        assert rec is not None and rec["oracle"] == "fast" and rec["config"] == c
+    assert bench.oracle_runstats("c3")["supersteps"] == 2 * 200_000 - 2   # chain: 2n-2
 
 
-def test_c1_known_supersteps_is_the_reference_run():
+def test_c1_runstats_are_the_reference_run():
     import _golden as G
-    got = G.c1()
-    if got is None:
-        pytest.skip("c1 fixture not generated")
-    assert bench.KNOWN_SUPERSTEPS["c1"] == got[0]["supersteps"]
+    meta, _ = G.c1()
+    rec = bench.oracle_runstats("c1")
+    assert (rec["supersteps"], rec["initial_blocks"], rec["final_blocks"]) == \
+        (meta["supersteps"], meta["initial_blocks"], meta["final_blocks"])
 
 
-@pytest.mark.gpu
-@pytest.mark.parametrize("config", ["c5", "c4l", "c1"])
-def test_known_supersteps_match_gpu(config):
-    inst, _ = bench.make_instance(config, 0)
-    if inst.kind == "bcrp":
-        block, st, _ = bcrp_arrays(inst.n, inst.src, inst.act, inst.dst, inst.num_actions)
-    else:
-        block, st, _ = rcpp_arrays(inst.n, inst.src, inst.dst, inst.pi0)
-    assert st.supersteps == bench.KNOWN_SUPERSTEPS[config]
-    if inst.truth is not None:
-        assert np.array_equal(block, inst.truth)
+def test_reference_arm_runs_and_matches_config():
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                          "--config", "c1", "--steps", "3", "--warmup", "1"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0
+    inst, desc = bench.make_instance("c1", 0)
+    assert line["config"] == bench.config_dict("c1", inst, desc, 1)
+    assert line["config"]["supersteps"] == 13962
+    assert line["cpu_baseline"]["kind"] == "port"
+    assert line["e2e"]["h2d_bytes_per_step"] == 0

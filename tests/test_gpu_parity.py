@@ -292,42 +292,40 @@ def test_c5_vlts_lifted_truth():
     assert st.final_block_count == len(np.unique(inst.truth))
 
 
-def test_label_grouping_equals_literal_rounds(monkeypatch):
+def test_label_grouping_equals_literal_rounds():
     """The hash-grouped label pre-partition equals the literal |Act| rounds
-    of bcrp.py:144-184 (BISIM_LITERAL_LABEL_ROUNDS forces the latter)."""
+    of bcrp.py:144-184 (FLAG_LITERAL_LABEL_ROUNDS forces the latter)."""
     for seed, (n, m, A) in enumerate([(3000, 9000, 5), (2000, 20000, 70), (5000, 5000, 200)]):
         g = np.random.default_rng(100 + seed)
         src = g.integers(0, n, m, dtype=np.int32)
         act = g.integers(0, A, m, dtype=np.int32)
         dst = g.integers(0, n, m, dtype=np.int32)
         b1, s1, _ = bcrp_arrays(n, src, act, dst, A)
-        monkeypatch.setenv("BISIM_LITERAL_LABEL_ROUNDS", "1")
-        b2, s2, _ = bcrp_arrays(n, src, act, dst, A)
-        monkeypatch.delenv("BISIM_LITERAL_LABEL_ROUNDS")
+        b2, s2, _ = bcrp_arrays(n, src, act, dst, A, flags=N.FLAG_LITERAL_LABEL_ROUNDS)
         assert np.array_equal(b1, b2) and s1 == s2
         assert np.array_equal(b1, oracle.bcrp(n, src, act, dst, A, threads=4).block)
 
 
-def test_noop_round_retirement_is_exact(monkeypatch):
+def test_noop_round_retirement_is_exact():
     """Retiring runs of no-op rounds (splitters whose in-edge sources all sit
     in singleton blocks) gives the same RunStats as running every round."""
     cases = [W.chain(3000), W.c2_kripke(n=20000, out_degree=3, seed=5),
              W.c4_uniform(n=20000, m=60000, num_actions=40, seed=6)]
     for inst in cases:
         if inst.kind == "bcrp":
-            run = lambda: bcrp_arrays(inst.n, inst.src, inst.act, inst.dst, inst.num_actions)
+            run = lambda f=0: bcrp_arrays(inst.n, inst.src, inst.act, inst.dst, inst.num_actions,
+                                          flags=f)
         else:
-            run = lambda: rcpp_arrays(inst.n, inst.src, inst.dst, inst.pi0)
+            run = lambda f=0: rcpp_arrays(inst.n, inst.src, inst.dst, inst.pi0, flags=f)
         b1, s1, n1 = run()
-        monkeypatch.setenv("BISIM_NO_SKIP", "1")
-        b2, s2, _ = run()
-        monkeypatch.delenv("BISIM_NO_SKIP")
+        b2, s2, _ = run(N.FLAG_NO_SKIP)
         assert np.array_equal(b1, b2), inst.name
         assert s1 == s2, inst.name
 
 
-@pytest.mark.parametrize("env", ["BISIM_NO_SOLO", "BISIM_NO_SKIP", "BISIM_CTA_MAJOR"])
-def test_loop_variants_identical(env, monkeypatch):
+@pytest.mark.parametrize("flag", ["FLAG_NO_SOLO", "FLAG_NO_SKIP", "FLAG_CTA_MAJOR",
+                                  "FLAG_NO_SOLO|FLAG_NO_SKIP"])
+def test_loop_variants_identical(flag):
     """Solo stretches, no-op retirement and work placement never change a
     result: every variant reproduces the oracle on mixed workloads."""
     insts = [W.c2_kripke(n=30000, out_degree=4, seed=8), W.fanout(2000),
@@ -339,13 +337,15 @@ def test_loop_variants_identical(env, monkeypatch):
     for inst in insts:
         if inst.kind == "bcrp":
             res = oracle.bcrp(inst.n, inst.src, inst.act, inst.dst, inst.num_actions, threads=8)
-            run = lambda: bcrp_arrays(inst.n, inst.src, inst.act, inst.dst, inst.num_actions)
+            run = lambda f=0: bcrp_arrays(inst.n, inst.src, inst.act, inst.dst, inst.num_actions,
+                                          flags=f)
         else:
             res = oracle.rcpp(inst.n, inst.src, inst.dst, inst.pi0, threads=8)
-            run = lambda: rcpp_arrays(inst.n, inst.src, inst.dst, inst.pi0)
+            run = lambda f=0: rcpp_arrays(inst.n, inst.src, inst.dst, inst.pi0, flags=f)
         b1, s1, _ = run()
         _same_oracle(b1, s1, res, inst.name)
-        monkeypatch.setenv(env, "1")
-        b2, s2, _ = run()
-        monkeypatch.delenv(env)
-        _same_oracle(b2, s2, res, inst.name + " " + env)
+        f = 0
+        for part in flag.split("|"):
+            f |= getattr(N, part)
+        b2, s2, _ = run(f)
+        _same_oracle(b2, s2, res, inst.name + " " + flag)

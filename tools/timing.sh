@@ -1,7 +1,7 @@
 #!/bin/bash
 # usage: tools/timing.sh c1 c5 ...   (one bench line per config, summarised)
 for c in "$@"; do
-  timeout 600 python bench.py --config $c --steps 2 --warmup 1 --no-cpu 2>&1 | tail -1 | python -c "
+  BISIM_DEV=1 timeout 600 python bench.py --config $c --steps 2 --warmup 1 --no-cpu 2>&1 | tail -1 | python -c "
 import json,sys
 t=sys.stdin.read()
 try:
