@@ -89,7 +89,25 @@ def main():
     ap.add_argument("--signature", action="store_true",
                     help="also record equality with the signature-refinement fixed point")
     ap.add_argument("configs", nargs="+")
+    ap.add_argument("--signature-only", action="store_true",
+                    help="add signature_equal to existing fixtures (compares digests)")
     a = ap.parse_args()
+    if a.signature_only:
+        import bench
+        from paper_2105_11788_b200 import workloads as W
+        for c in a.configs:
+            path = os.path.join(OUT, f"{c}.{a.oracle}.json")
+            with open(path) as fh:
+                rec = json.load(fh)
+            inst, _ = bench.make_instance(c, 0)
+            act = inst.act if inst.kind == "bcrp" else np.zeros(inst.m, np.int32)
+            truth = W.signature_bisim(inst.n, inst.src, act, inst.dst,
+                                      init=None if inst.kind == "bcrp" else inst.pi0)
+            rec["signature_equal"] = sha(truth) == rec["block_sha256"]
+            with open(path, "w") as fh:
+                json.dump(rec, fh, indent=1)
+            print(c, rec["signature_equal"], flush=True)
+        return
     for c in a.configs:
         rec = run(c, a.oracle, a.threads, a.signature)
         print(json.dumps(rec), flush=True)

@@ -153,8 +153,11 @@ def partition_by_outgoing_labels(lts, policy, *, common_election: bool | None = 
     _check_policy(policy, common_election)
     n, src, act, _, A = lts_columns(lts)
     block = np.empty(n, np.int32)
-    N.check(N.lib().bisim_label_partition(n, src.size, A, N.ptr(src), N.ptr(act), N.ptr(block),
-                                          device))
+    rc = N.lib().bisim_label_partition(n, src.size, A, N.ptr(src), N.ptr(act), N.ptr(block),
+                                       device)
+    if rc == N.BISIM_BAD_INPUT:
+        raise ValueError(N.last_error())
+    N.check(rc)
     return Partition(block, _trusted=True)
 
 

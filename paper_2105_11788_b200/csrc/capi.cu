@@ -16,6 +16,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/bisim.h"
@@ -74,6 +75,8 @@ struct Ctx {
         small_list, big_list, big_base, tmp, scnt, smin, kcur, scur, counter, brange, bar, trace, lhash, lkeys,
         lmins, sarr, big_list4, big_base4, big_info, big_info4, sinfo, nrm;
     int launches = 0;
+    struct Stager* stager = nullptr;  // pinned staging of pageable host arrays (lazy)
+    ~Ctx();
 };
 
 std::mutex g_ctx_mu;
@@ -117,6 +120,137 @@ std::unique_ptr<Ctx> make_ctx(int device) {
         c->grid_sparse_rcpp = occupancy_grid((const void*)k_refine_sparse<true, false>, c->sms, kSparseThreads, 1);
         return c;
     }
+}
+
+// ---- host <-> device copies of caller arrays ------------------------------
+//
+// Pinned (page-locked) host arrays go straight to cudaMemcpyAsync.  Pageable
+// arrays -- what a Python caller normally passes -- are staged: the array is
+// split over T worker threads, each owning two pinned chunk buffers and a
+// stream; a worker memcpy's chunk k into one buffer while the DMA of chunk
+// k-1 drains from the other, so T host copies run beside the DMA engine
+// instead of the driver's single staging pipeline.
+struct Stager {
+    static constexpr size_t kChunk = 8u << 20;
+    int T = 0;
+    std::vector<void*> buf;             // 2 per worker
+    std::vector<cudaStream_t> streams;  // 1 per worker
+    std::vector<cudaEvent_t> done;      // 2 per worker (buffer free again)
+    std::vector<cudaEvent_t> fin;       // 1 per worker
+    cudaEvent_t start = nullptr;
+};
+
+Stager& stager(Ctx& c) {
+    if (c.stager) return *c.stager;
+    auto* S = new Stager();
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    S->T = (int)std::max(1u, std::min(8u, hw / 2));
+    S->buf.resize(2 * S->T);
+    S->streams.resize(S->T);
+    S->done.resize(2 * S->T);
+    S->fin.resize(S->T);
+    for (auto& b : S->buf) CK(cudaHostAlloc(&b, Stager::kChunk, cudaHostAllocPortable));
+    for (auto& st : S->streams) CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    for (auto& e : S->done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : S->fin) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&S->start, cudaEventDisableTiming));
+    c.stager = S;
+    return *S;
+}
+
+Ctx::~Ctx() {
+    // errors are ignored: at process exit the runtime may already be gone
+    cudaSetDevice(device);
+    if (stager) {
+        for (void* b : stager->buf) cudaFreeHost(b);
+        for (auto st : stager->streams) cudaStreamDestroy(st);
+        for (auto e : stager->done) cudaEventDestroy(e);
+        for (auto e : stager->fin) cudaEventDestroy(e);
+        if (stager->start) cudaEventDestroy(stager->start);
+        delete stager;
+    }
+    for (auto& e : ev)
+        if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+}
+
+bool host_pinned(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
+
+// Staged copy of `bytes` between host `h` and device `d` (dir = H2D / D2H),
+// ordered after the work already queued on `st`; on return the copies are
+// queued (H2D) or complete (D2H), and `st` waits for them.
+void staged_copy(Ctx& c, void* d, void* h, size_t bytes, cudaMemcpyKind dir, cudaStream_t st) {
+    if (bytes < (size_t)4 * Stager::kChunk || host_pinned(h)) {
+        CK(cudaMemcpyAsync(dir == cudaMemcpyHostToDevice ? d : h, dir == cudaMemcpyHostToDevice ? h : d, bytes,
+                           dir, st));
+        if (dir == cudaMemcpyDeviceToHost) CK(cudaStreamSynchronize(st));
+        return;
+    }
+    Stager& S = stager(c);
+    CK(cudaEventRecord(S.start, st));
+    const size_t per = ((bytes + S.T - 1) / S.T + 4095) & ~(size_t)4095;
+    std::vector<cudaError_t> err(S.T, cudaSuccess);
+    auto work = [&](int t) {
+        cudaError_t e = cudaSetDevice(c.device);
+        cudaStream_t ws = S.streams[t];
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(ws, S.start, 0);
+        const size_t lo = std::min(bytes, (size_t)t * per), hi = std::min(bytes, lo + per);
+        size_t prev_off = 0, prev_len = 0;
+        int k = 0;
+        for (size_t off = lo; off < hi && e == cudaSuccess; off += Stager::kChunk, ++k) {
+            const size_t len = std::min(Stager::kChunk, hi - off);
+            const int slot = 2 * t + (k & 1);
+            char* b = (char*)S.buf[slot];
+            if (dir == cudaMemcpyHostToDevice) {
+                e = cudaEventSynchronize(S.done[slot]);  // the DMA out of this buffer finished
+                if (e != cudaSuccess) break;
+                memcpy(b, (const char*)h + off, len);
+                e = cudaMemcpyAsync((char*)d + off, b, len, dir, ws);
+                if (e == cudaSuccess) e = cudaEventRecord(S.done[slot], ws);
+            } else {
+                e = cudaMemcpyAsync(b, (const char*)d + off, len, dir, ws);
+                if (e == cudaSuccess) e = cudaEventRecord(S.done[slot], ws);
+                if (e == cudaSuccess && k > 0) {  // drain the previous chunk while this one flies
+                    const int ps = 2 * t + ((k - 1) & 1);
+                    e = cudaEventSynchronize(S.done[ps]);
+                    if (e == cudaSuccess) memcpy((char*)h + prev_off, S.buf[ps], prev_len);
+                }
+                prev_off = off;
+                prev_len = len;
+            }
+        }
+        if (e == cudaSuccess && dir == cudaMemcpyDeviceToHost && prev_len) {
+            const int ps = 2 * t + ((k - 1) & 1);
+            e = cudaEventSynchronize(S.done[ps]);
+            if (e == cudaSuccess) memcpy((char*)h + prev_off, S.buf[ps], prev_len);
+        }
+        if (e == cudaSuccess) e = cudaEventRecord(S.fin[t], ws);
+        err[t] = e;
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < S.T; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th : pool) th.join();
+    for (int t = 0; t < S.T; ++t) {
+        if (err[t] != cudaSuccess) CK(err[t]);
+        CK(cudaStreamWaitEvent(st, S.fin[t], 0));
+    }
+}
+
+void h2d(Ctx& c, void* d, const void* h, size_t bytes, cudaStream_t st) {
+    if (bytes) staged_copy(c, d, const_cast<void*>(h), bytes, cudaMemcpyHostToDevice, st);
+}
+
+// Complete on return.
+void d2h(Ctx& c, void* h, const void* d, size_t bytes, cudaStream_t st) {
+    if (bytes) staged_copy(c, const_cast<void*>(d), h, bytes, cudaMemcpyDeviceToHost, st);
 }
 
 int grid_for(int64_t work, int threads, int sms) {
@@ -298,11 +432,9 @@ LabelTables label_tables(Ctx& c, int32_t n, int64_t m, int32_t A, const int32_t*
     int32_t* d_src = (int32_t*)c.src.ensure(mm * 4);
     int32_t* d_act = (int32_t*)c.act.ensure(mm * 4);
     int32_t* d_dst = dst ? (int32_t*)c.dst.ensure(mm * 4) : d_src;
-    if (m) {
-        CK(cudaMemcpyAsync(d_src, src, m * 4, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(d_act, act, m * 4, cudaMemcpyHostToDevice, st));
-        if (dst) CK(cudaMemcpyAsync(d_dst, dst, m * 4, cudaMemcpyHostToDevice, st));
-    }
+    h2d(c, d_src, src, m * 4, st);
+    h2d(c, d_act, act, m * 4, st);
+    if (dst) h2d(c, d_dst, dst, m * 4, st);
     Ctrl* ctrl = (Ctrl*)c.ctrl.ensure(std::max(sizeof(Ctrl), sizeof(SCtrl)));
     t.lmask = (unsigned long long*)c.lmask.ensure((size_t)W * n * 8);
     CK(cudaMemsetAsync(ctrl, 0, sizeof(Ctrl), st));
@@ -377,16 +509,14 @@ int run_with(Ctx& c, Job& j) {
     } else {
         d_src = (int32_t*)c.src.ensure(mm * 4);
         d_dst = (int32_t*)c.dst.ensure(mm * 4);
-        if (m) {
-            CK(cudaMemcpyAsync((void*)d_src, j.src, m * 4, cudaMemcpyHostToDevice, st));
-            CK(cudaMemcpyAsync((void*)d_dst, j.dst, m * 4, cudaMemcpyHostToDevice, st));
-        }
+        h2d(c, (void*)d_src, j.src, m * 4, st);
+        h2d(c, (void*)d_dst, j.dst, m * 4, st);
         if (j.bcrp) {
             d_act = (int32_t*)c.act.ensure(mm * 4);
-            if (m) CK(cudaMemcpyAsync((void*)d_act, j.act, m * 4, cudaMemcpyHostToDevice, st));
+            h2d(c, (void*)d_act, j.act, m * 4, st);
         } else {
             d_pi0 = (int32_t*)c.pi0.ensure((int64_t)n * 4);
-            CK(cudaMemcpyAsync((void*)d_pi0, j.pi0, (int64_t)n * 4, cudaMemcpyHostToDevice, st));
+            h2d(c, (void*)d_pi0, j.pi0, (int64_t)n * 4, st);
         }
     }
     CK(cudaEventRecord(c.ev[1], st));
@@ -721,7 +851,7 @@ int run_with(Ctx& c, Job& j) {
     if (j.block_out_on_device)
         CK(cudaMemcpyAsync(j.block_out, block, (int64_t)n * 4, cudaMemcpyDeviceToDevice, st));
     else
-        CK(cudaMemcpyAsync(j.block_out, block, (int64_t)n * 4, cudaMemcpyDeviceToHost, st));
+        d2h(c, j.block_out, block, (int64_t)n * 4, st);
     const int64_t R = ls.round;
     const int64_t ncopy = std::min<int64_t>(std::min<int64_t>(R, j.splits_cap), splits_dev_cap);
     if (j.splits_out && ncopy > 0)
@@ -846,7 +976,7 @@ int run_sharded(Job& base, const int32_t* devices, int G, int32_t flags) {
     {
         const int64_t mm = std::max<int64_t>(m, 1);
         int32_t* d_src = (int32_t*)c0.src.ensure(mm * 4);
-        if (m) CK(cudaMemcpyAsync(d_src, base.src, m * 4, cudaMemcpyHostToDevice, c0.stream));
+        h2d(c0, d_src, base.src, m * 4, c0.stream);
         lo = shard_bounds(c0, n, m, d_src, G);
     }
     // every replica: inputs, preprocessing, label partition, loop state

@@ -306,6 +306,7 @@ __device__ __forceinline__ void raise_flush_warp0(const SparseParams& p, int cur
             s_u2[lane] = 0u;
         }
     }
+    __syncwarp();  // every lane has read s_nsplit / s_ndirty before lane 0 resets them
     if (lane == 0) {
         red_min(&p.ctrl->next_min[cur], s_nmin);
         if (round < p.splits_cap) red_add(&p.splits[round], ns);

@@ -335,12 +335,10 @@ int bisim_quotient(int32_t n, int64_t m, int32_t num_actions, const int32_t* src
         int32_t* d_act = (int32_t*)c.act.ensure(mm * 4);
         int32_t* d_dst = (int32_t*)c.dst.ensure(mm * 4);
         int32_t* d_block = (int32_t*)c.block.ensure((int64_t)n * 4);
-        if (m) {
-            CK(cudaMemcpyAsync(d_src, src, m * 4, cudaMemcpyHostToDevice, st));
-            CK(cudaMemcpyAsync(d_act, act, m * 4, cudaMemcpyHostToDevice, st));
-            CK(cudaMemcpyAsync(d_dst, dst, m * 4, cudaMemcpyHostToDevice, st));
-        }
-        CK(cudaMemcpyAsync(d_block, block, (int64_t)n * 4, cudaMemcpyHostToDevice, st));
+        h2d(c, d_src, src, m * 4, st);
+        h2d(c, d_act, act, m * 4, st);
+        h2d(c, d_dst, dst, m * 4, st);
+        h2d(c, d_block, block, (int64_t)n * 4, st);
         check_transitions(c, n, m, num_actions, d_src, d_act, d_dst);
         // leader index: dense numbering of the leaders in increasing order
         int32_t* qidx = (int32_t*)c.bstart.ensure(((int64_t)n + 1) * 4);
@@ -401,12 +399,10 @@ int bisim_is_stable(int32_t n, int64_t m, int32_t num_actions, const int32_t* sr
         int32_t* d_act = (int32_t*)c.act.ensure(mm * 4);
         int32_t* d_dst = (int32_t*)c.dst.ensure(mm * 4);
         int32_t* d_block = (int32_t*)c.block.ensure((int64_t)n * 4);
-        if (m) {
-            CK(cudaMemcpyAsync(d_src, src, m * 4, cudaMemcpyHostToDevice, st));
-            CK(cudaMemcpyAsync(d_act, act, m * 4, cudaMemcpyHostToDevice, st));
-            CK(cudaMemcpyAsync(d_dst, dst, m * 4, cudaMemcpyHostToDevice, st));
-        }
-        CK(cudaMemcpyAsync(d_block, block, (int64_t)n * 4, cudaMemcpyHostToDevice, st));
+        h2d(c, d_src, src, m * 4, st);
+        h2d(c, d_act, act, m * 4, st);
+        h2d(c, d_dst, dst, m * 4, st);
+        h2d(c, d_block, block, (int64_t)n * 4, st);
         check_transitions(c, n, m, num_actions, d_src, d_act, d_dst);
         int32_t* bad = (int32_t*)c.counter.ensure(16);
         int32_t* flags = (int32_t*)c.bstart.ensure(((int64_t)n + 1) * 4);
@@ -456,12 +452,10 @@ int bisim_is_stable_under(int32_t n, int64_t m, int32_t num_actions, const int32
         int32_t* d_dst = (int32_t*)c.dst.ensure(mm * 4);
         int32_t* d_block = (int32_t*)c.block.ensure((int64_t)n * 4);
         int32_t* d_states = (int32_t*)c.pi0.ensure(std::max<int64_t>(num_states, 1) * 4);
-        if (m) {
-            CK(cudaMemcpyAsync(d_src, src, m * 4, cudaMemcpyHostToDevice, st));
-            CK(cudaMemcpyAsync(d_act, act, m * 4, cudaMemcpyHostToDevice, st));
-            CK(cudaMemcpyAsync(d_dst, dst, m * 4, cudaMemcpyHostToDevice, st));
-        }
-        CK(cudaMemcpyAsync(d_block, block, (int64_t)n * 4, cudaMemcpyHostToDevice, st));
+        h2d(c, d_src, src, m * 4, st);
+        h2d(c, d_act, act, m * 4, st);
+        h2d(c, d_dst, dst, m * 4, st);
+        h2d(c, d_block, block, (int64_t)n * 4, st);
         if (num_states) CK(cudaMemcpyAsync(d_states, states, num_states * 4, cudaMemcpyHostToDevice, st));
         check_transitions(c, n, m, num_actions, d_src, d_act, d_dst);
         int32_t* bad = (int32_t*)c.counter.ensure(16);

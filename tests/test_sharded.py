@@ -109,3 +109,37 @@ def test_sharded_rejects_bad_shard_counts():
         bcrp_sharded_arrays(2, z, z, z, 1, [0] * 9)
     with pytest.raises(ValueError):
         bcrp_sharded_arrays(2, z, z, z, 1, [])
+
+
+def _device_count():
+    from paper_2105_11788_b200 import _native as N
+    return int(N.lib().bisim_device_count())
+
+
+@pytest.mark.parametrize("g", [2, 4, 8])
+def test_sharded_distinct_devices(g):
+    """The cross-device branch: peer access between distinct GPUs, the
+    cooperative launch per device and the system-scope barrier over NVLink
+    (capi.cu run_sharded).  Runs only on a machine with >= g GPUs."""
+    if _device_count() < g:
+        pytest.skip(f"needs {g} GPUs (this machine has {_device_count()})")
+    devices = list(range(g))
+    cases = G.cases()
+    for name in ("fanout_64", "chain_200", "pre_fig2"):
+        rec = cases[name]
+        n, src, act, dst, A = G.arrays(rec)
+        block, st, _ = bcrp_sharded_arrays(n, src, act, dst, A, devices, verify=True)
+        _same(block, st, rec["bcrp"], f"{name} x{g} devices")
+    inst = W.lifted_quotient(400_000, 2000, 32, 6, 3, 2, seed=12)
+    ref_block, ref_st, _ = bcrp_arrays(inst.n, inst.src, inst.act, inst.dst, inst.num_actions)
+    block, st, _ = bcrp_sharded_arrays(inst.n, inst.src, inst.act, inst.dst, inst.num_actions,
+                                       devices, verify=True)
+    assert np.array_equal(block, inst.truth) and np.array_equal(block, ref_block)
+    assert st == ref_st
+
+
+def test_sharded_rejects_out_of_range_sources():
+    with pytest.raises(ValueError):
+        bcrp_sharded_arrays(3, [0, 5], [0, 0], [1, 2], 1, [0, 0])
+    block, st, _ = bcrp_sharded_arrays(3, [0, 1], [0, 0], [1, 2], 1, [0, 0])
+    assert list(block) == [0, 1, 2]
