@@ -73,7 +73,7 @@ struct Ctx {
     DevBuf src, act, dst, pi0, lmask, off, rev_ptr, cursor, rev_slot, block, nl, mark, unstable,
         split_list, cmem, splits, ctrl, scan_tmp, rev2, members, bstart, bsize, tblock,
         small_list, big_list, big_base, tmp, scnt, smin, kcur, scur, counter, brange, bar, trace, lhash, lkeys,
-        lmins, sarr, big_list4, big_base4, big_info, big_info4, sinfo, nrm;
+        lmins, sarr, big_list4, big_base4, big_info, big_info4, sinfo, nrm, bcur, stage;
     int launches = 0;
     struct Stager* stager = nullptr;  // pinned staging of pageable host arrays (lazy)
     ~Ctx();
@@ -461,6 +461,30 @@ LabelTables label_tables(Ctx& c, int32_t n, int64_t m, int32_t A, const int32_t*
     return t;
 }
 
+// Reverse CSR fill (sparse modes): bucketed staging pass + in-order placement
+// (kernels_sparse.cuh k_rev_bucket / k_rev_place).  cursor = copy of rev_ptr.
+template <bool BCRP>
+void rev_fill_bucketed(Ctx& c, int32_t n, int64_t m, const int32_t* d_src, const int32_t* d_act,
+                       const int32_t* d_dst, const unsigned long long* lmask, const int32_t* off,
+                       const int4* sinfo, const int32_t* rev_ptr, int32_t* cursor, int2* rev2, int32_t* rev_src,
+                       int32_t src_lo, int32_t src_hi) {
+    cudaStream_t st = c.stream;
+    int shift = 0;
+    while (((int64_t)n >> shift) >= 256) ++shift;  // <= 256 buckets
+    const int32_t nb = (int32_t)(((int64_t)n - 1) >> shift) + 1;
+    int32_t* bcur = (int32_t*)c.bcur.ensure((int64_t)nb * 4);
+    int4* stage = (int4*)c.stage.ensure(std::max<int64_t>(m, 1) * 16);
+    k_bucket_init<<<(nb + 255) / 256, 256, 0, st>>>(n, shift, nb, rev_ptr, bcur);
+    const int64_t tiles = (m + kBucketTile - 1) / kBucketTile;
+    const int g1 = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)c.sms * 4));
+    k_rev_bucket<BCRP><<<g1, kBucketThreads, 0, st>>>(n, m, d_src, d_act, d_dst, lmask, off, sinfo, shift, nb, bcur,
+                                                      stage, src_lo, src_hi);
+    // staged in-edges: rev_ptr[n] <= m of them (only sources in [src_lo, src_hi))
+    k_rev_place<BCRP><<<grid_for(m, 256, c.sms), 256, 0, st>>>(rev_ptr + n, stage, cursor, rev2, rev_src);
+    c.launches += 3;
+    CK(cudaGetLastError());
+}
+
 int run_with(Ctx& c, Job& j);
 
 int run(Job& j) { return run_with(*get_ctx(j.opt.device), j); }
@@ -597,11 +621,11 @@ int run_with(Ctx& c, Job& j) {
                 k_pack_sinfo<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, lmask, off, sinfo);
                 ++c.launches;
             }
-            k_rev_fill2<true><<<g, TB, 0, st>>>(n, m, d_src, d_act, d_dst, lmask, off, cursor, rev2, nullptr,
-                                                src_lo, src_hi, sinfo);
+            rev_fill_bucketed<true>(c, n, m, d_src, d_act, d_dst, lmask, off, sinfo, rev_ptr, cursor, rev2, nullptr,
+                                    src_lo, src_hi);
         } else {
-            k_rev_fill2<false><<<g, TB, 0, st>>>(n, m, d_src, d_act, d_dst, lmask, off, cursor, nullptr, rev_src,
-                                                 src_lo, src_hi, nullptr);
+            rev_fill_bucketed<false>(c, n, m, d_src, d_act, d_dst, lmask, off, nullptr, rev_ptr, cursor, nullptr,
+                                     rev_src, src_lo, src_hi);
         }
         ++c.launches;
     }
@@ -669,7 +693,8 @@ int run_with(Ctx& c, Job& j) {
         int32_t* bstart = (int32_t*)c.bstart.ensure(((int64_t)n + 1) * 4);
         int32_t* bsize = (int32_t*)c.bsize.ensure((int64_t)n * 4);
         CK(cudaMemsetAsync(bstart, 0, ((int64_t)n + 1) * 4, st));
-        k_block_sizes<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, block, bstart);
+        const int ggrid = std::max(1, std::min(c.sms * 4, (int)((n + kGroupThreads - 1) / kGroupThreads)));
+        k_group_states<false><<<ggrid, kGroupThreads, 0, st>>>(n, block, bstart, nullptr, nullptr, nullptr);
         ++c.launches;
         CK(cudaMemcpyAsync(bsize, bstart, (int64_t)n * 4, cudaMemcpyDeviceToDevice, st));
         scan_excl(c, bstart, n);
@@ -677,8 +702,8 @@ int run_with(Ctx& c, Job& j) {
         int2* brange = (int2*)c.brange.ensure((int64_t)n * 8);
         k_pack_ranges<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, bstart, bsize, brange);
         ++c.launches;
-        k_fill_members<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, block, cursor, j.bcrp ? off : nullptr, rev_ptr,
-                                                              members);
+        k_group_states<true><<<ggrid, kGroupThreads, 0, st>>>(n, block, cursor, j.bcrp ? off : nullptr, rev_ptr,
+                                                             members);
         ++c.launches;
         uint32_t* U1 = U + nw0;
         uint32_t* U2 = U1 + nw1 + 1;

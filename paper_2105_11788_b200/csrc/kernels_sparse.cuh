@@ -796,4 +796,167 @@ __global__ void k_rev_fill2(int32_t n, int64_t m, const int32_t* __restrict__ sr
     }
 }
 
+
+// ---- reverse CSR fill in two bucketed passes ----------------------------------
+//
+// The one-pass fill (k_rev_fill2) scatters 8-byte in-edges to random
+// positions of an m-entry array far larger than L2: every 32-byte sector is
+// fetched and written back several times (~0.25 KB of DRAM traffic per
+// transition).  Here transitions are first grouped by target bucket (a range
+// of 2^shift targets) into a staging array laid out like rev itself (bucket
+// b starts at rev_ptr[b << shift]), with one global reservation per (tile,
+// bucket); the second pass walks the staging array in order, so the
+// positions it scatters to lie in the one or two buckets being worked on --
+// a few MB that stay in L2 until their sectors are complete.
+constexpr int kBucketThreads = 512;
+constexpr int kBucketItems = 8;                        // transitions per thread per tile
+constexpr int kBucketTile = kBucketThreads * kBucketItems;
+constexpr int kMaxBuckets = 1024;
+
+__global__ void k_bucket_init(int32_t n, int shift, int32_t nb, const int32_t* __restrict__ rev_ptr, int32_t* bcur) {
+    for (int32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x)
+        bcur[b] = rev_ptr[min((int64_t)b << shift, (int64_t)n)];
+}
+
+template <bool BCRP>
+__global__ void __launch_bounds__(kBucketThreads) k_rev_bucket(
+    int32_t n, int64_t m, const int32_t* __restrict__ src, const int32_t* __restrict__ act,
+    const int32_t* __restrict__ dst, const unsigned long long* __restrict__ lmask,
+    const int32_t* __restrict__ off, const int4* __restrict__ sinfo, int shift, int32_t nb, int32_t* bcur,
+    int4* stage, int32_t lo, int32_t hi) {
+    __shared__ int32_t cnt[kMaxBuckets];
+    __shared__ int32_t base[kMaxBuckets];
+    for (int64_t t0 = (int64_t)blockIdx.x * kBucketTile; t0 < m; t0 += (int64_t)gridDim.x * kBucketTile) {
+        for (int b = threadIdx.x; b < nb; b += blockDim.x) cnt[b] = 0;
+        __syncthreads();
+        int32_t t[kBucketItems], slot[kBucketItems], s[kBucketItems], r[kBucketItems];
+#pragma unroll
+        for (int k = 0; k < kBucketItems; ++k) {
+            const int64_t i = t0 + k * kBucketThreads + threadIdx.x;
+            t[k] = -1;
+            if (i < m) {
+                s[k] = src[i];
+                if (s[k] >= lo && s[k] < hi) t[k] = dst[i];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kBucketItems; ++k) {
+            if (t[k] < 0) continue;
+            const int64_t i = t0 + k * kBucketThreads + threadIdx.x;
+            if (!BCRP) {
+                slot[k] = s[k];
+            } else if (sinfo) {
+                const int4 q = sinfo[s[k]];
+                const unsigned long long w = ((unsigned long long)(uint32_t)q.y << 32) | (uint32_t)q.x;
+                slot[k] = q.z + __popcll(w & ((1ull << (act[i] & 63)) - 1ull));
+            } else {
+                slot[k] = off[s[k]] + label_rank(lmask, n, s[k], act[i]);
+            }
+            r[k] = atomicAdd(&cnt[t[k] >> shift], 1);
+        }
+        __syncthreads();
+        for (int b = threadIdx.x; b < nb; b += blockDim.x)
+            if (cnt[b]) base[b] = atomicAdd(&bcur[b], cnt[b]);
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kBucketItems; ++k)
+            if (t[k] >= 0) stage[base[t[k] >> shift] + r[k]] = make_int4(t[k], slot[k], s[k], 0);
+        __syncthreads();
+    }
+}
+
+template <bool BCRP>
+__global__ void k_rev_place(const int32_t* __restrict__ ptotal, const int4* __restrict__ stage, int32_t* cursor,
+                            int2* rev, int32_t* rev_src) {
+    const int lane = threadIdx.x & 31;
+    const int64_t total = *ptotal;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < total;
+         i0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = i0 + lane;
+        int4 q = make_int4(-1 - lane, 0, 0, 0);
+        if (i < total) q = __ldcs(&stage[i]);
+        const LaneRun run = lane_run(q.x);
+        int32_t at = 0;
+        if (i < total && run.rank == 0) at = atomicAdd(&cursor[q.x], run.len);
+        at = __shfl_sync(kFull, at, run.leader) + run.rank;
+        if (i < total) {
+            if (BCRP) rev[at] = make_int2(q.y, q.z);
+            else rev_src[at] = q.z;
+        }
+    }
+}
+
+// ---- states grouped by block, with CTA-level aggregation -----------------------
+//
+// After the label pre-partition a handful of blocks may hold all n states
+// (c5: 8): per-warp atomics on their counters serialise in L2.  Each CTA
+// counts a tile of states per block in a shared hash table and reserves its
+// run of every block with one global atomic; a tile with too many distinct
+// blocks for the table falls back to per-warp atomics.
+constexpr int kGroupThreads = 512;
+constexpr int kGroupTable = 512;       // hash slots (power of two)
+
+__device__ __forceinline__ int group_slot(int32_t* keys, int32_t b) {
+    uint32_t h = ((uint32_t)b * 2654435761u) >> 23;  // 9 bits
+#pragma unroll 1
+    for (int probe = 0; probe < 32; ++probe) {
+        const int32_t old = atomicCAS(&keys[h], -1, b);
+        if (old == -1 || old == b) return (int)h;
+        h = (h + 1) & (kGroupTable - 1);
+    }
+    return -1;
+}
+
+// FILL = false: bsize[b] += members of b.  FILL = true: members of b go to
+// cursor[b] ... (cursor advanced), as member records.
+template <bool FILL>
+__global__ void __launch_bounds__(kGroupThreads) k_group_states(
+    int32_t n, const int32_t* __restrict__ block, int32_t* counter, const int32_t* __restrict__ off,
+    const int32_t* __restrict__ rev_ptr, MemberRec* members) {
+    __shared__ int32_t keys[kGroupTable];
+    __shared__ int32_t cnt[kGroupTable];
+    __shared__ int32_t base[kGroupTable];
+    __shared__ int overflow;
+    const int lane = threadIdx.x & 31;
+    for (int64_t t0 = (int64_t)blockIdx.x * kGroupThreads; t0 < n; t0 += (int64_t)gridDim.x * kGroupThreads) {
+        for (int k = threadIdx.x; k < kGroupTable; k += blockDim.x) {
+            keys[k] = -1;
+            cnt[k] = 0;
+        }
+        if (threadIdx.x == 0) overflow = 0;
+        __syncthreads();
+        const int64_t s = t0 + threadIdx.x;
+        const int32_t b = s < n ? block[s] : -1 - lane;
+        const unsigned g = __match_any_sync(kFull, b);
+        const int leader = __ffs(g) - 1;
+        int slot = -1, r = 0;
+        if (s < n && lane == leader) {
+            slot = group_slot(keys, b);
+            if (slot >= 0) r = atomicAdd(&cnt[slot], __popc(g));
+            else overflow = 1;
+        }
+        __syncthreads();
+        const bool ovf = overflow != 0;
+        if (!ovf) {
+            for (int k = threadIdx.x; k < kGroupTable; k += blockDim.x)
+                if (cnt[k]) {
+                    const int32_t v = atomicAdd(&counter[keys[k]], cnt[k]);
+                    if (FILL) base[k] = v;
+                }
+        } else if (s < n && lane == leader) {  // crowded tile: per-warp runs
+            r = atomicAdd(&counter[b], __popc(g));
+        }
+        __syncthreads();
+        if (FILL) {
+            int32_t at = 0;
+            if (s < n && lane == leader) at = ovf ? r : base[slot] + r;
+            at = __shfl_sync(kFull, at, leader);
+            if (s < n)
+                members[at + __popc(g & lanemask_lt())] =
+                    make_int4((int32_t)s, off ? off[s] : 0, rev_ptr[s], rev_ptr[s + 1]);
+        }
+        __syncthreads();
+    }
+}
+
 }  // namespace bisim
