@@ -479,8 +479,15 @@ void rev_fill_bucketed(Ctx& c, int32_t n, int64_t m, const int32_t* d_src, const
     const int g1 = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)c.sms * 4));
     k_rev_bucket<BCRP><<<g1, kBucketThreads, 0, st>>>(n, m, d_src, d_act, d_dst, lmask, off, sinfo, shift, nb, bcur,
                                                       stage, src_lo, src_hi);
-    // staged in-edges: rev_ptr[n] <= m of them (only sources in [src_lo, src_hi))
-    k_rev_place<BCRP><<<grid_for(m, 256, c.sms), 256, 0, st>>>(rev_ptr + n, stage, cursor, rev2, rev_src);
+    // staged in-edges: rev_ptr[n] <= m of them (only sources in [src_lo, src_hi)).
+    // Exactly the resident number of CTAs: the grid-stride sweep then moves
+    // through the staging array as one wave, so the rev positions being
+    // written stay within a few MB (an oversubscribed grid sweeps twice,
+    // half a window each time, and the sectors leave L2 half-written).
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k_rev_place<BCRP>, 256, 0));
+    const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c.sms * std::max(occ, 1), (m + 255) / 256));
+    k_rev_place<BCRP><<<g2, 256, 0, st>>>(rev_ptr + n, stage, cursor, rev2, rev_src);
     c.launches += 3;
     CK(cudaGetLastError());
 }
