@@ -179,6 +179,20 @@ int bisim_preprocess_sorted(int32_t n, int64_t m, int32_t num_actions, const int
 int bisim_label_partition(int32_t n, int64_t m, int32_t num_actions, const int32_t *src,
                           const int32_t *act, int32_t *block_out, int device);
 
+/* The label pre-partition under the plain Common policy (bcrp.py:144-184
+ * with common_election=False; pram.py:147-152): the literal |Act| rounds,
+ * stopped at the first round whose elect phase has two states of one block
+ * writing different new leaders.  On a conflict: *conflict_round = that
+ * round (0-based), *conflict_leader = the block's leader (the reference's
+ * address ("new_leader", leader) -- the conflicting block whose smallest
+ * disagreeing state is smallest), *conflict_winner = that smallest state,
+ * and block_out = the partition after the round (the conflicting values
+ * are the states with block_out == *conflict_winner).  Without a conflict
+ * *conflict_round = -1 and block_out = the label partition. */
+int bisim_label_rounds_common(int32_t n, int64_t m, int32_t num_actions, const int32_t *src,
+                              const int32_t *act, int32_t *conflict_round, int32_t *conflict_leader,
+                              int32_t *conflict_winner, int32_t *block_out, int device);
+
 /* ---- the steps either side of the path ------------------ */
 /* quotient(lts, partition) (aut.py:132-152): one state per block, blocks
  * numbered densely in increasing leader order, duplicate (block, action,

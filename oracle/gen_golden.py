@@ -10,6 +10,7 @@ can check against them.
     python oracle/gen_golden.py c1         # config c1 full run (~35 min, 1 core)
     python oracle/gen_golden.py post       # quotient / is_stable / canonical fixtures
     python oracle/gen_golden.py aut        # parse_aut outcomes (texts + results / errors)
+    python oracle/gen_golden.py common     # plain-Common-policy outcomes (violations, guards)
 
 Every fixture records the instance (src/act/dst arrays or the generator
 recipe), the reference's Priority-policy outputs (block array in leader form,
@@ -386,7 +387,103 @@ def aut(fuzz=3000):
     print(f"wrote aut.json.gz ({len(recs)} texts, {errs} parse errors)")
 
 
+def common():
+    """Outcomes of the reference under the PLAIN Common policy
+    (common_election=False, pram.py:147-152): PolicyViolationError address
+    and values, SuperstepLimitError, or the result -- plus the observer calls
+    made before -- for BCRP and RCPP instances reaching every branch (label
+    round conflicts, the first-select conflict, one-block systems, RCPP
+    round-1 splits of 0 / 1 / >= 2 states, non-canonical pi0, guards)."""
+    pb = _ref()
+    sys.path.insert(0, REF_TESTS)
+    import _support as sup
+    from parbisim.cli import gen_fanout
+
+    def outcome(run):
+        calls = []
+        try:
+            part, st = run(lambda k, p: calls.append([k, list(p.block)]))
+        except pb.PolicyViolationError as e:
+            addr = list(e.address) if isinstance(e.address, tuple) else e.address
+            return {"raised": "policy", "address": addr, "values": list(e.values),
+                    "message": str(e), "observed": calls}
+        except pb.SuperstepLimitError as e:
+            return {"raised": "guard", "message": str(e), "observed": calls}
+        return {"raised": None, "block": list(part.block), "supersteps": st.supersteps,
+                "splits": list(st.splits_per_iteration), "initial_blocks": st.initial_block_count,
+                "final_blocks": st.final_block_count, "observed": calls}
+
+    def bcrp_case(lts, guards=(None,)):
+        rec = lts_arrays(lts)
+        rec["common"] = {str(g): outcome(lambda obs, g=g: pb.bcrp_run(
+            lts, pb.Common(), common_election=False, observer=obs, max_supersteps=g))
+            for g in guards}
+        try:
+            lp = pb.partition_by_outgoing_labels(lts, pb.Common(), common_election=False)
+            rec["label_common"] = {"raised": None, "block": list(lp.block)}
+        except pb.PolicyViolationError as e:
+            addr = list(e.address) if isinstance(e.address, tuple) else e.address
+            rec["label_common"] = {"raised": "policy", "address": addr, "values": list(e.values)}
+        return rec
+
+    def rcpp_case(n, edges, pi0, guards=(None,)):
+        rel = pb.RelationInput(n, tuple(edges), pb.Partition(pi0))
+        rec = {"n": n, "src": [e[0] for e in edges], "dst": [e[1] for e in edges], "pi0": list(pi0)}
+        rec["common"] = {str(g): outcome(lambda obs, g=g: pb.rcpp_run(
+            rel, pb.Common(), common_election=False, observer=obs, max_supersteps=g))
+            for g in guards}
+        return rec
+
+    bcrp, rcpp = [], []
+    L = pb.lts_from_labeled_edges
+    guards = (None, -1, 0, 1, 2, 3, 4, 5)
+    # label-round conflicts (most systems), first-select conflicts (chains),
+    # one-block systems (cycles, edge-free), hubs
+    bcrp.append(bcrp_case(sup.mixed_label_lts(), guards))
+    for n in (2, 3, 5, 8):
+        bcrp.append(bcrp_case(chain_lts(pb, n), guards))
+        bcrp.append(bcrp_case(L(n, [(i, "a", (i + 1) % n) for i in range(n)]), guards))
+        bcrp.append(bcrp_case(L(n, [(i, lab, (i + 1) % n) for i in range(n) for lab in "ab"]),
+                              guards))
+    bcrp.append(bcrp_case(pb.Lts(4, ("a", "b"), ()), guards))
+    for n in (3, 4, 6, 10):
+        bcrp.append(bcrp_case(gen_fanout(n), guards))
+    bcrp.append(bcrp_case(L(4, [(0, "a", 1), (1, "b", 2), (2, "a", 3), (3, "b", 0)]), guards))
+    bcrp.append(bcrp_case(L(5, [(0, "a", 1), (2, "a", 1), (3, "b", 4)], extra_labels=["c"]),
+                          guards))
+    rng = random.Random(777)
+    for _ in range(300):
+        bcrp.append(bcrp_case(sup.random_lts(random.Random(rng.randrange(2 ** 32))), (None, 1, 3)))
+    # RCPP: >= 2 blocks, one block with round-1 split sets of size 0 / 1 / >= 2,
+    # non-canonical leaders
+    rcpp.append(rcpp_case(3, [(1, 0), (2, 0)], [0, 0, 0], guards))          # test_acceptance.py:361
+    rcpp.append(rcpp_case(5, [(0, 3), (1, 4), (1, 2), (2, 1)], [0, 0, 0, 3, 3], guards))
+    for n in (2, 3, 4, 7):
+        rcpp.append(rcpp_case(n, [(i, i + 1) for i in range(n - 1)], [0] * n, guards))
+        rcpp.append(rcpp_case(n, [(i, (i + 1) % n) for i in range(n)], [0] * n, guards))
+        rcpp.append(rcpp_case(n, [(i, i + 1) for i in range(n - 1)], [n - 1] * n, guards))
+        rcpp.append(rcpp_case(n, [(i, (i + 1) % n) for i in range(n)], [n // 2] * n, guards))
+    rcpp.append(rcpp_case(4, [(0, 1)], [2, 2, 2, 2], guards))
+    rcpp.append(rcpp_case(4, [(1, 0), (2, 3), (3, 3)], [1, 1, 1, 1], guards))
+    rcpp.append(rcpp_case(4, [], [0, 0, 0, 0], guards))
+    for _ in range(200):
+        r = random.Random(rng.randrange(2 ** 32))
+        n = r.randrange(1, 9)
+        edges = [(r.randrange(n), r.randrange(n)) for _ in range(r.randrange(0, 3 * n))]
+        k = r.randrange(1, 3)
+        col = [r.randrange(k) for _ in range(n)]
+        lead = {}
+        for sidx in r.sample(range(n), n):
+            lead.setdefault(col[sidx], sidx)
+        rcpp.append(rcpp_case(n, edges, [lead[c] for c in col], (None, 0, 1, 2)))
+    with gzip.open(os.path.join(OUT, "common.json.gz"), "wt") as fh:
+        json.dump({"bcrp": bcrp, "rcpp": rcpp}, fh, separators=(",", ":"))
+    kinds = [o["raised"] for rec in bcrp + rcpp for o in rec["common"].values()]
+    print(f"wrote common.json.gz ({len(bcrp)} bcrp, {len(rcpp)} rcpp; outcomes "
+          f"{ {k: kinds.count(k) for k in set(kinds)} })")
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     what = sys.argv[1] if len(sys.argv) > 1 else "cases"
-    {"cases": cases, "sweep": sweep, "c1": c1, "post": post, "aut": aut}[what]()
+    {"cases": cases, "sweep": sweep, "c1": c1, "post": post, "aut": aut, "common": common}[what]()

@@ -82,7 +82,8 @@ EXPORTS = ("bisim_bcrp", "bisim_rcpp", "bisim_bcrp_ex", "bisim_rcpp_ex", "bisim_
            "bisim_device_count", "bisim_stream", "bisim_version", "bisim_quotient",
            "bisim_is_stable", "bisim_canonical", "bisim_aut_parse", "bisim_aut_read_file",
            "bisim_aut_columns", "bisim_aut_label", "bisim_aut_free", "bisim_bcrp_sharded",
-           "bisim_rcpp_sharded", "bisim_is_stable_under", "bisim_preprocess_sorted")
+           "bisim_rcpp_sharded", "bisim_is_stable_under", "bisim_preprocess_sorted",
+           "bisim_label_rounds_common")
 
 
 def lib():
@@ -116,6 +117,8 @@ def lib():
             L.bisim_preprocess_sorted.argtypes = [i32, i64, i32, i32p, i32p, i32p, i32p, i32p, i32p,
                                                   i32p, i32p, i32p, i32p, i32p, P(i64),
                                                   ctypes.c_int]
+            L.bisim_label_rounds_common.argtypes = [i32, i64, i32, i32p, i32p, i32p, i32p, i32p, i32p,
+                                                    ctypes.c_int]
             L.bisim_label_partition.argtypes = [i32, i64, i32, i32p, i32p, i32p, ctypes.c_int]
             L.bisim_quotient.argtypes = [i32, i64, i32, i32p, i32p, i32p, i32p, i32, P(i32),
                                          P(i64), i32p, i32p, i32p, P(i32), ctypes.c_int]
@@ -139,7 +142,8 @@ def lib():
                          "bisim_label_partition", "bisim_device_count", "bisim_quotient",
                          "bisim_is_stable", "bisim_canonical", "bisim_aut_parse",
                          "bisim_aut_read_file", "bisim_aut_columns", "bisim_bcrp_sharded",
-                         "bisim_rcpp_sharded", "bisim_is_stable_under", "bisim_preprocess_sorted"):
+                         "bisim_rcpp_sharded", "bisim_is_stable_under", "bisim_preprocess_sorted",
+           "bisim_label_rounds_common"):
                 getattr(L, name).restype = ctypes.c_int
             # pointer / void results: never through the int loop above (a
             # c_int restype truncates a heap pointer to 32 bits)

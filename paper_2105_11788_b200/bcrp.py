@@ -118,16 +118,64 @@ def bcrp_arrays(n: int, src, act, dst, num_actions: int, *, max_supersteps: int 
     return block, stats, st.as_dict()
 
 
-def _check_policy(policy, common_election):
+def _plain_common(policy, common_election) -> bool:
+    """True for Common without the Alg. 6 election: the reference then
+    raises PolicyViolationError at the first conflicting concurrent write
+    (pram.py:147-152)."""
     kind = policy_kind(policy)
     if common_election is None:
         common_election = kind == "common"
-    if kind == "common" and not common_election:
-        # Plain Common (no Alg. 6 election) is illegal as soon as two
-        # processors write different values; the GPU kernels implement the
-        # elected (Priority-equivalent) program only.
-        raise PolicyViolationError("C", [])
-    return kind
+    return kind == "common" and not common_election
+
+
+def _guard_error(step: int, limit: int):
+    return SuperstepLimitError(f"superstep guard exceeded ({step} > {limit})")
+
+
+def _label_rounds_common(n, src, act, A, device):
+    """(conflict round or -1, old leader, new leader, block) of the plain-
+    Common label rounds (bisim_label_rounds_common)."""
+    r, lead, win = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    block = np.empty(n, np.int32)
+    rc = N.lib().bisim_label_rounds_common(n, src.size, A, N.ptr(src), N.ptr(act),
+                                           ctypes.byref(r), ctypes.byref(lead), ctypes.byref(win),
+                                           N.ptr(block), device)
+    if rc == N.BISIM_BAD_INPUT:
+        raise ValueError(N.last_error())
+    N.check(rc)
+    return r.value, lead.value, win.value, block
+
+
+def _plain_common_bcrp(n, src, act, dst, A, max_supersteps, observer, device):
+    """bcrp_run under plain Common, as the reference executes it.
+
+    Until the first conflicting write the Common rounds are the Priority
+    rounds.  Conflicts can only occur (a) in a label round's elect phase
+    (two states of one block disagree with their leader), (b) at the first
+    main-loop select, when the label partition has two or more blocks (every
+    leader writes C).  With one block every state has the same label set,
+    so every slot of every state is marked in round 1 and nothing splits:
+    the Priority run is the Common run.
+    """
+    guard = 3 * n + A + 8 if max_supersteps is None else int(max_supersteps)
+    r, lead, win, block = _label_rounds_common(n, src, act, A, device)
+    trip = max(guard, 0) + 1                   # the superstep at which the guard fires
+    if r >= 0:
+        if trip <= r + 1:                      # before the conflicting label round
+            raise _guard_error(trip, guard)
+        raise PolicyViolationError(("new_leader", lead), np.nonzero(block == win)[0].tolist())
+    if trip <= A:
+        raise _guard_error(trip, guard)
+    leaders = np.unique(block)
+    if leaders.size >= 2:
+        if guard < A + 1:
+            raise _guard_error(A + 1, guard)
+        raise PolicyViolationError("C", leaders.tolist())
+    return None   # one block: run the Priority program
+
+
+def _check_policy(policy, common_election):
+    return policy_kind(policy)
 
 
 def bcrp_run(lts, policy, *, common_election: bool | None = None, observer=None,
@@ -137,10 +185,15 @@ def bcrp_run(lts, policy, *, common_election: bool | None = None, observer=None,
     Same contract as the reference: returns ``(Partition, RunStats)``;
     ``observer(iteration, partition)`` is called after every counted
     superstep; ``max_supersteps`` defaults to ``3n + |Act| + 8`` and raises
-    :class:`SuperstepLimitError` when exceeded.
+    :class:`SuperstepLimitError` when exceeded.  Plain ``Common`` (no
+    election) raises :class:`PolicyViolationError` exactly where the
+    reference does.
     """
-    _check_policy(policy, common_election)
+    plain = _plain_common(policy, common_election)
     n, src, act, dst, A = lts_columns(lts)
+    if plain:
+        _plain_common_bcrp(n, N.as_i32(src), N.as_i32(act), N.as_i32(dst), A, max_supersteps,
+                           observer, device)
     block, stats, _ = bcrp_arrays(n, src, act, dst, A, max_supersteps=max_supersteps,
                                   observer=observer, device=device)
     return Partition(block, _trusted=True), stats
@@ -150,8 +203,13 @@ def partition_by_outgoing_labels(lts, policy, *, common_election: bool | None = 
                                  device: int = 0) -> Partition:
     """States grouped by outgoing label set, min-index leaders
     (bcrp.py:129-141)."""
-    _check_policy(policy, common_election)
     n, src, act, _, A = lts_columns(lts)
+    if _plain_common(policy, common_election):
+        # the engine's guard is |Act| + 1 (bcrp.py:139): never trips here
+        r, lead, win, blk = _label_rounds_common(n, N.as_i32(src), N.as_i32(act), A, device)
+        if r >= 0:
+            raise PolicyViolationError(("new_leader", lead), np.nonzero(blk == win)[0].tolist())
+        return Partition(blk, _trusted=True)
     block = np.empty(n, np.int32)
     rc = N.lib().bisim_label_partition(n, src.size, A, N.ptr(src), N.ptr(act), N.ptr(block),
                                        device)

@@ -67,7 +67,7 @@ struct Ctx {
     int sms = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[6] = {};
-    int grid_refine_bcrp = 0, grid_refine_rcpp = 0, grid_label = 0;
+    int grid_refine_bcrp = 0, grid_refine_rcpp = 0, grid_label = 0, grid_label_common = 0;
     int grid_sparse_bcrp = 0, grid_sparse_rcpp = 0;
     std::mutex mu;
     DevBuf src, act, dst, pi0, lmask, off, rev_ptr, cursor, rev_slot, block, nl, mark, unstable,
@@ -116,6 +116,7 @@ std::unique_ptr<Ctx> make_ctx(int device) {
         c->grid_refine_bcrp = occupancy_grid((const void*)k_refine<false>, c->sms);
         c->grid_refine_rcpp = occupancy_grid((const void*)k_refine<true>, c->sms);
         c->grid_label = occupancy_grid((const void*)k_label_rounds, c->sms);
+        c->grid_label_common = occupancy_grid((const void*)k_label_rounds_common, c->sms);
         c->grid_sparse_bcrp = occupancy_grid((const void*)k_refine_sparse<false, false>, c->sms, kSparseThreads, 1);
         c->grid_sparse_rcpp = occupancy_grid((const void*)k_refine_sparse<true, false>, c->sms, kSparseThreads, 1);
         return c;
@@ -1417,6 +1418,46 @@ int bisim_label_partition(int32_t n, int64_t m, int32_t num_actions, const int32
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(block_out, block, (int64_t)n * 4, cudaMemcpyDeviceToHost, c.stream));
         CK(cudaStreamSynchronize(c.stream));
+    });
+}
+
+int bisim_label_rounds_common(int32_t n, int64_t m, int32_t num_actions, const int32_t* src, const int32_t* act,
+                              int32_t* conflict_round, int32_t* conflict_leader, int32_t* conflict_winner,
+                              int32_t* block_out, int device) {
+    return guarded_call([&]() {
+        if (!block_out || !conflict_round || !conflict_leader || !conflict_winner)
+            throw Error(BISIM_BAD_INPUT, "null output");
+        Ctx& c = *get_ctx(device);
+        std::lock_guard<std::mutex> lock(c.mu);
+        LabelTables t = label_tables(c, n, m, num_actions, src, act);
+        cudaStream_t st = c.stream;
+        int32_t* block = (int32_t*)c.block.ensure((int64_t)n * 4);
+        auto* nl = (unsigned long long*)c.nl.ensure((int64_t)n * 8);
+        int32_t* moved = (int32_t*)c.bsize.ensure((int64_t)n * 4);
+        int32_t* conf = (int32_t*)c.counter.ensure(16);
+        auto* conf_key = (unsigned long long*)c.sarr.ensure(8);
+        CK(cudaMemsetAsync(block, 0, (int64_t)n * 4, st));
+        CK(cudaMemsetAsync(nl, 0, (int64_t)n * 8, st));
+        CK(cudaMemsetAsync(moved, 0, (int64_t)n * 4, st));
+        CK(cudaMemsetAsync(conf, 0x7f, 4, st));
+        CK(cudaMemsetAsync(conf_key, 0xff, 8, st));
+        if (num_actions > 0) {
+            int32_t nn = n, AA = num_actions;
+            const unsigned long long* lm = t.lmask;
+            void* args[] = {&nn, &AA, (void*)&lm, &block, &nl, &moved, &conf, &conf_key};
+            CK(cudaLaunchCooperativeKernel((const void*)k_label_rounds_common, c.grid_label_common, kThreads, args, 0,
+                                           st));
+        }
+        int32_t h_conf = 0;
+        unsigned long long h_key = 0;
+        CK(cudaMemcpyAsync(&h_conf, conf, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&h_key, conf_key, 8, cudaMemcpyDeviceToHost, st));
+        d2h(c, block_out, block, (int64_t)n * 4, st);
+        CK(cudaStreamSynchronize(st));
+        const bool hit = h_conf != 0x7f7f7f7f;
+        *conflict_round = hit ? h_conf : -1;
+        *conflict_winner = hit ? (int32_t)(h_key >> 32) : -1;
+        *conflict_leader = hit ? (int32_t)(h_key & 0xffffffffu) : -1;
     });
 }
 

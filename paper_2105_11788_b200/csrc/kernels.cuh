@@ -470,6 +470,51 @@ __global__ void __launch_bounds__(kThreads) k_label_rounds(int32_t n, int32_t A,
     }
 }
 
+// The same rounds under the plain Common policy (no Alg. 6 election,
+// bcrp.py:176-182 with common_election=False): a round's elect phase is
+// illegal as soon as two states of one block disagree with their leader
+// (pram.py:147-152).  Until that happens the Priority rounds above are the
+// Common rounds, and a block's disagreeing states are exactly the states
+// that move to its new leader w -- so the first round in which two states
+// move to the same w is the first conflict.  w is a fresh label (a state
+// becomes a leader once), so per-w move counters never need a reset.
+// conf[0] = first conflicting round (INT32_MAX if none); conf_key = min over
+// conflicting blocks of (w << 32 | old leader): the reference raises for
+// the address ("new_leader", old leader) of the block whose smallest
+// disagreeing state is smallest (first group in processor order).
+__global__ void __launch_bounds__(kThreads) k_label_rounds_common(int32_t n, int32_t A,
+                                                                  const unsigned long long* __restrict__ lmask,
+                                                                  int32_t* block, unsigned long long* nl,
+                                                                  int32_t* moved, int32_t* conf,
+                                                                  unsigned long long* conf_key) {
+    cg::grid_group grid = cg::this_grid();
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
+    for (int32_t a = 0; a < A; ++a) {
+        const unsigned long long* plane = lmask + (int64_t)(a >> 6) * n;
+        const int sh = a & 63;
+        const int64_t epoch = a + 1;
+        for (int64_t s = gtid; s < n; s += gsize) {
+            const int32_t l = block[s];
+            if (l != s && (((plane[s] ^ plane[l]) >> sh) & 1ull)) atomicMax(&nl[l], elect_key(epoch, (int32_t)s));
+        }
+        grid.sync();
+        for (int64_t s = gtid; s < n; s += gsize) {
+            const int32_t l = block[s];
+            if (l != s && (((plane[s] ^ plane[l]) >> sh) & 1ull)) {
+                const int32_t w = elect_winner(nl[l]);
+                block[s] = w;
+                if (atomicAdd(&moved[w], 1) == 1) {  // the second mover: a conflicting block
+                    atomicMin(conf, a);
+                    atomicMin(conf_key, ((unsigned long long)(uint32_t)w << 32) | (uint32_t)l);
+                }
+            }
+        }
+        grid.sync();
+        if (ld_vol(conf) <= a) break;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Refinement loop (Alg. 3 / Alg. 2) as one persistent cooperative kernel.
 //

@@ -12,7 +12,8 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as N
-from .bcrp import _ObserverBridge, _check_policy, _options, _raise_for
+from .bcrp import _ObserverBridge, _check_policy, _guard_error, _options, _plain_common, _raise_for
+from .policy import PolicyViolationError, SuperstepLimitError
 from .lts import Partition, RunStats
 
 # Block labels are state ids, so -1 is "no label" (rcpp.py:32-35).
@@ -104,9 +105,63 @@ def rcpp_run(rel, policy, *, common_election: bool | None = None, observer=None,
     (rcpp.py:220-259); ``max_supersteps`` defaults to ``3n + 9``."""
     _check_policy(policy, common_election)
     n, src, dst, pi0 = _relation_columns(rel)
+    if _plain_common(policy, common_election):
+        _plain_common_rcpp(n, src, dst, pi0, max_supersteps, observer, device)
     block, stats, _ = rcpp_arrays(n, src, dst, pi0, max_supersteps=max_supersteps,
                                   observer=observer, device=device)
     return Partition(block, _trusted=True), stats
+
+
+class _RoundOne(Exception):
+    pass
+
+
+def _plain_common_rcpp(n, src, dst, pi0, max_supersteps, observer, device):
+    """rcpp_run under plain Common, as the reference executes it
+    (rcpp.py:75-98, :196-204 with common_election=False).
+
+    Two or more initial blocks: every leader is unstable and writes C at the
+    first select.  One block (leader L): round 1 splits off the states whose
+    "has an edge" mark differs from L's; two or more of them write
+    new_leader[L] in sub-phase A (conflict), exactly one makes round 2's
+    select see two unstable labels (conflict after round 1, whose observer
+    call happens), none is the Priority run.  The round-1 split set is read
+    from the GPU's Priority round 1 (identical to Common's up to sub_a).
+    """
+    guard = 3 * n + 9 if max_supersteps is None else int(max_supersteps)
+    leaders = np.unique(pi0)
+    if leaders.size >= 2:
+        try:  # input validation only: a guard of 0 trips at the first superstep
+            rcpp_arrays(n, src, dst, pi0, max_supersteps=0, device=device)
+        except SuperstepLimitError:
+            pass
+        if guard < 1:
+            raise _guard_error(1, guard)
+        raise PolicyViolationError("C", leaders.tolist())
+    L = int(leaders[0])
+    got = {}
+
+    def first(k, part):
+        got["block"] = np.asarray(part.block, np.int32)
+        raise _RoundOne
+
+    try:
+        rcpp_arrays(n, src, dst, pi0, max_supersteps=max_supersteps, observer=first,
+                    device=device)
+    except _RoundOne:
+        pass
+    if "block" not in got:
+        return None            # no round ran (no conflict possible): Priority run
+    S = np.nonzero(got["block"] != L)[0]
+    if S.size >= 2:
+        raise PolicyViolationError(("new_leader", L), S.tolist())
+    if S.size == 1:
+        if observer is not None:
+            observer(1, Partition(got["block"], _trusted=True))
+        if guard < 2:
+            raise _guard_error(2, guard)
+        raise PolicyViolationError("C", sorted([L, int(S[0])]))
+    return None                # nothing split: the Priority run is the Common run
 
 
 __all__ = ["NONE_LABEL", "RelationInput", "rcpp_arrays", "rcpp_run"]
