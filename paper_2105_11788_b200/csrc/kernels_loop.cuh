@@ -40,8 +40,13 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
     // SH (transition-sharded replica, kernels_shard.cuh): the round-parity
     // buffers are selected per round on a local copy of the parameters;
     // otherwise p is the kernel parameter itself
-    SparseParams pl;
-    if (SH) pl = pk;
+    // (in shared memory: a local copy would live on the stack, 700+ bytes)
+    __shared__ SparseParams s_pl;
+    SparseParams& pl = s_pl;
+    if (SH) {
+        if (threadIdx.x == 0) pl = pk;
+        __syncthreads();
+    }
     const SparseParams& p = SH ? pl : pk;
     SCtrl* ctl = p.ctrl;
     unsigned xgen = 0;  // cross-replica barriers passed (SH)
@@ -335,15 +340,10 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
 #pragma unroll
                     for (int u = 0; u < kA; ++u) {
                         s[u] = rv[u].y;
+                        const int32_t slot = IDENT ? s[u] : rv[u].x;
                         if (act[u]) {
-                            if (IDENT) {
-                                if (SH) shard_mark(p, cur, s[u]);
-                                else red_or(&p.mark[s[u] >> 5], 1u << (s[u] & 31));
-                            } else if (SH) {
-                                shard_mark(p, cur, rv[u].x);
-                            } else {
-                                red_or(&p.mark[rv[u].x >> 5], 1u << (rv[u].x & 31));
-                            }
+                            if (SH) shard_mark(p, cur, slot);
+                            else red_or(&p.mark[slot >> 5], 1u << (slot & 31));
                         }
                         b[u] = act[u] ? p.block[s[u]] : 0;
                     }

@@ -33,12 +33,20 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
     return v;
 }
 
+// pl is the CTA's shared copy of the parameters: every thread reads it, so
+// thread 0 switches the pointers between two CTA barriers.
 __device__ __forceinline__ void shard_select_parity(SparseParams& pl, const SparseParams& pk, int cur) {
-    pl.mark = pk.mark + cur * pk.mark_stride;
-    pl.tblock = pk.tblock + cur * pk.bm_stride;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        pl.mark = pk.mark + cur * pk.mark_stride;
+        pl.tblock = pk.tblock + cur * pk.bm_stride;
+    }
+    __syncthreads();
 }
 
-// Mark slot `slot` in every replica.
+// Mark slot `slot` in every replica.  (Combining the bits of lanes that hit
+// the same word first -- match_any + reduce_or -- measured slower: BCRP and
+// RCPP mark slots of one warp step rarely share a word.)
 __device__ __forceinline__ void shard_mark(const SparseParams& p, int cur, int32_t slot) {
     const int64_t mo = cur * p.mark_stride + (slot >> 5);
     const uint32_t mb = 1u << (slot & 31);
