@@ -79,6 +79,9 @@ __device__ __forceinline__ void red_and(uint32_t* a, uint32_t v) {
 __device__ __forceinline__ void red_min(int32_t* a, int32_t v) {
     asm volatile("red.relaxed.gpu.global.min.s32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
 }
+__device__ __forceinline__ void red_min_u32(uint32_t* a, uint32_t v) {
+    asm volatile("red.relaxed.gpu.global.min.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
 __device__ __forceinline__ void red_add(int32_t* a, int32_t v) {
     asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
 }

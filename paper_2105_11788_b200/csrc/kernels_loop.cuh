@@ -75,7 +75,16 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
         ctl->nontriv[0] = ctl->nontriv[1] = kBig;
         ctl->skipcnt[0] = ctl->skipcnt[1] = 0;
         ctl->items_last = kBig;
+        for (int q = 0; q < 2; ++q) {
+            ctl->brec[q][0] = 0u;
+            ctl->brec[q][1] = ~0u;
+            ctl->brec[q][2] = ctl->brec[q][3] = 0u;
+            ctl->arec[q][0] = ctl->arec[q][1] = ctl->arec[q][2] = ctl->arec[q][3] = 0u;
+            ctl->big_pack4[q] = 0ull;
+        }
     }
+    unsigned genB0 = 0u, genB1 = 0u;  // end-of-round barriers passed, by parity (uniform)
+    unsigned genA0 = 0u, genA1 = 0u;  // mid-round barriers passed, by parity (uniform)
     grid_barrier(p.bar, gen);
     int32_t C = ld_vol(&ctl->C0);
     int64_t round = ld_vol(&ctl->round);
@@ -186,6 +195,14 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
                 if (cand && !round_is_trivial<IDENT>(p, c)) atomicMin(&ctl->nontriv[sp], c);
             }
             team_barrier(solo, p.bar, gen, [&] { s_snap[0] = ld_vol(&ctl->nontriv[sp]); });
+            if (ttid == 0) {  // the round after the skip may have either parity
+                for (int q = 0; q < 2; ++q) {
+                    ctl->brec[q][1] = ~0u;
+                    ctl->brec[q][2] = ctl->brec[q][3] = 0u;
+                    ctl->arec[q][1] = ctl->arec[q][2] = ctl->arec[q][3] = 0u;
+                    ctl->big_pack4[q] = 0ull;
+                }
+            }
             const int32_t nt = (int32_t)s_snap[0];
             const int32_t end = min(nt, lim);
             int32_t cnt = 0;
@@ -249,14 +266,14 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
             const int32_t sc = u_clear_next_warp(p, C);
             int2 sr = make_int2(0, 0);
             if (lane == 0) {
-                ctl->succ[cur] = sc;
-                ctl->next_min[cur] = kBig;
                 // the usual next splitter: fetch its member range now (it
-                // cannot change this round unless the label is raised again)
-                if (sc != kBig) {
-                    sr = p.brange[sc];
-                    ctl->succ_range[cur] = sr;
-                }
+                // cannot change this round unless the label is raised again);
+                // both go into this round's end-of-round record
+                if (sc != kBig) sr = p.brange[sc];
+                unsigned* rec = ctl->brec[cur];
+                red_or(&rec[2], (unsigned)sr.x);
+                red_or(&rec[3], (unsigned)sr.y);
+                red_min_u32(&rec[1], ((unsigned)sc << 1) | 1u);
                 if (solo) {
                     s_succ = sc;
                     s_succ_range = sr;
@@ -409,25 +426,49 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
             if (!shard_exchange(p, cur, gen, xgen, s_snap)) break;
             shard_merge(p, cur, tw, tnw, s_snap);
         }
-        team_barrier(solo, p.bar, gen, [&] {
-            if (solo) {
+        if (solo) {
+            team_barrier(true, p.bar, gen, [&] {
                 s_snap[0] = s_ctr_nsmall;
                 s_snap[1] = (long long)s_ctr_big;
                 s_snap[2] = (long long)s_ctr_big4;
                 s_ctr_nsmall = 0;  // the phase-A counters of the next solo round
                 s_ctr_big = s_ctr_big4 = 0ull;
-            } else {
-                s_snap[0] = ld_vol(&ctl->n_small[cur]);
-                s_snap[1] = (long long)ld_vol(&ctl->big_pack[cur]);
-                s_snap[2] = (long long)ld_vol(&ctl->big_pack4[cur]);
+            });
+        } else {
+            // mid-round barrier on this parity's record: the poll that sees
+            // every arrival also returns the registration counters; the wide
+            // layout's chunk count is loaded only when the layout choice
+            // below needs it
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                unsigned* rec = ctl->arec[cur];
+                const unsigned target = ((cur ? genA1 : genA0) + 1u) * gridDim.x;
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(rec) : "memory");
+                unsigned w0, w1, w2, w3;
+                do {
+                    asm volatile(
+                        "{\n\t.reg .b128 t;\n\tld.acquire.gpu.global.b128 t, [%4];\n\t"
+                        "mov.b128 {%0, %1, %2, %3}, t;\n\t}"
+                        : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
+                        : "l"(rec)
+                        : "memory");
+                } while ((int)(w0 - target) < 0);
+                s_snap[0] = (int32_t)w1;
+                s_snap[1] = (long long)(((unsigned long long)w3 << 32) | w2);
+                const int32_t nb = (int32_t)w3, n1 = (int32_t)w2, tw_all = (int32_t)(blockDim.x >> 5) * gridDim.x;
+                const bool need4 = n1 > tw_all || n1 > 512 * nb || p.wide_major > 0 || p.force_mode_b > 0;
+                s_snap[2] = need4 ? (long long)ld_vol(&ctl->big_pack4[cur]) : 0ll;
             }
-        });
+            if (cur) ++genA1;
+            else ++genA0;
+            __syncthreads();
+        }
         if (tr) {
             p.trace[round * kTraceWords + 2] = globaltimer();
             p.trace[round * kTraceWords + 4] = p.brange[C].y;
             p.trace[round * kTraceWords + 5] = solo ? 1 : 0;
-            p.trace[round * kTraceWords + 6] = ld_vol(&ctl->n_small[cur]);
-            p.trace[round * kTraceWords + 7] = ld_vol(&ctl->big_pack[cur]);
+            p.trace[round * kTraceWords + 6] = s_snap[0];
+            p.trace[round * kTraceWords + 7] = s_snap[1];
         }
 
         // ---- phase B: split the touched blocks ------------------------------
@@ -437,15 +478,15 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
         const int32_t nbig = (int32_t)(bp >> 32), nch1 = (int32_t)(bp & 0xffffffffu);
         const int32_t nch4 = (int32_t)(bp4 & 0xffffffffu);
         if (ttid == 0) {
-            ctl->n_small[nxt] = 0;
-            ctl->big_pack[nxt] = 0ull;
+            ctl->arec[nxt][1] = 0u;
+            ctl->arec[nxt][2] = ctl->arec[nxt][3] = 0u;
             ctl->big_pack4[nxt] = 0ull;
-            ctl->heavy[nxt] = 0;
-            ctl->csplit[nxt] = 0;
-            ctl->items_last = nsm + nch1;
-            s_items_last = nsm + nch1;
+            ctl->brec[nxt][1] = ~0u;  // the next round's record (its parity's last
+            ctl->brec[nxt][2] = 0u;   // readers passed this round's first barrier)
+            ctl->brec[nxt][3] = 0u;
             if (SH) p.peer_xcnt[p.shard][nxt] = 0;
         }
+        if (threadIdx.x == 0) s_items_last = nsm + nch1;
         // chunk layout and pass count for this round (kernels_big.cuh)
         // one pass needs a warp per big-block chunk only: small blocks are
         // independent items that any warp takes on the side
@@ -492,42 +533,67 @@ __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParam
             if (lane == 0) my_members += (unsigned long long)cnt;
         }
         for (int k = threadIdx.x; k < kSeen; k += blockDim.x) s_seen[k] = -1;
-        team_barrier(solo, p.bar, gen, [&] { raise_flush_warp0(p, cur, round); }, [&] {
-            int32_t nm, sc, sx, sy, cs;
-            if (solo) {  // everything this round raised or found is in this CTA
-                nm = s_nmin_round;
-                cs = s_csplit_round;
-                sc = s_succ;
-                sx = s_succ_range.x;
-                sy = s_succ_range.y;
+        if (solo) {
+            team_barrier(true, p.bar, gen, [&] { raise_flush_warp0(p, cur, round); }, [&] {
+                // everything this round raised or found is in this CTA
+                const int32_t nm = s_nmin_round, cs = s_csplit_round, sc = s_succ;
                 s_snap[4] = s_ctr_heavy;
                 s_ctr_heavy = 0;
                 s_snap[5] = s_items_last;
-            } else {
-                nm = ld_vol(&ctl->next_min[cur]);
-                cs = ld_vol(&ctl->csplit[cur]);
-                sc = ld_vol(&ctl->succ[cur]);
-                const int32_t* sr = (const int32_t*)&ctl->succ_range[cur];
-                sx = ld_vol(sr);
-                sy = ld_vol(sr + 1);
-                s_snap[4] = ld_vol(&ctl->heavy[cur]);
-                s_snap[5] = ld_vol(&ctl->items_last);
-            }
-            const int32_t c_next = min(nm, sc);
-            s_snap[3] = c_next;
-            if (c_next != kBig) {
-                if (nm > sc) {
-                    s_snap[6] = ((long long)sy << 32) | (unsigned)sx;
-                } else if (!kNoCsnap && c_next == C && !cs) {
-                    // C raised again (BCRP re-raise) without splitting: its
-                    // range is unchanged, no dependent load
-                    s_snap[6] = ((long long)cr.y << 32) | (unsigned)cr.x;
-                } else {
-                    const int32_t* r = (const int32_t*)&p.brange[c_next];
-                    s_snap[6] = ((long long)ld_vol(r + 1) << 32) | (unsigned)ld_vol(r);
+                const int32_t c_next = min(nm, sc);
+                s_snap[3] = c_next;
+                if (c_next != kBig) {
+                    if (nm > sc) {
+                        s_snap[6] = ((long long)s_succ_range.y << 32) | (unsigned)s_succ_range.x;
+                    } else if (!kNoCsnap && c_next == C && !cs) {
+                        s_snap[6] = ((long long)cr.y << 32) | (unsigned)cr.x;
+                    } else {
+                        const int32_t* r = (const int32_t*)&p.brange[c_next];
+                        s_snap[6] = ((long long)ld_vol(r + 1) << 32) | (unsigned)ld_vol(r);
+                    }
+                }
+            });
+        } else {
+            // end-of-round barrier on this parity's record: the poll that
+            // sees every arrival also returns the next splitter (min of the
+            // raised labels and C's successor), the successor's range and the
+            // round's flags -- no separate load of the control words after it
+            __syncthreads();
+            if (threadIdx.x < 32) raise_flush_warp0(p, cur, round);
+            if (threadIdx.x == 0) {
+                unsigned* rec = ctl->brec[cur];
+                const unsigned target = ((cur ? genB1 : genB0) + 1u) * gridDim.x;
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(rec) : "memory");
+                unsigned w0, w1, w2, w3;
+                do {
+                    asm volatile(
+                        "{\n\t.reg .b128 t;\n\tld.acquire.gpu.global.b128 t, [%4];\n\t"
+                        "mov.b128 {%0, %1, %2, %3}, t;\n\t}"
+                        : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
+                        : "l"(rec)
+                        : "memory");
+                } while ((int)(w0 - target) < 0);
+                const int32_t c_next = (int32_t)(w1 >> 1);  // ~0u -> kBig
+                s_snap[3] = c_next;
+                s_snap[4] = (w2 & kRecFlag) ? 1 : 0;
+                s_snap[5] = s_items_last;
+                if (c_next != kBig) {
+                    if (w1 & 1u) {  // the successor, not raised this round
+                        s_snap[6] = ((long long)(w3 & ~kRecFlag) << 32) | (w2 & ~kRecFlag);
+                    } else if (!kNoCsnap && c_next == C && !(w3 & kRecFlag)) {
+                        // C raised again (BCRP re-raise) without splitting: its
+                        // range is unchanged, no dependent load
+                        s_snap[6] = ((long long)cr.y << 32) | (unsigned)cr.x;
+                    } else {
+                        const int32_t* r = (const int32_t*)&p.brange[c_next];
+                        s_snap[6] = ((long long)ld_vol(r + 1) << 32) | (unsigned)ld_vol(r);
+                    }
                 }
             }
-        });
+            if (cur) ++genB1;
+            else ++genB0;
+            __syncthreads();
+        }
         if (tr) p.trace[round * kTraceWords + 3] = globaltimer();
         C = (int32_t)s_snap[3];
         if (C != kBig) {

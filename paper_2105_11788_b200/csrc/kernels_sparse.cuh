@@ -123,7 +123,21 @@ struct SCtrl {
     int32_t items_last;                 // phase-B work items of the last round
     int32_t pub_try_skip, pub_cooldown, pub_backoff, pad2;
     int64_t pub_skips;
+    // End-of-round barrier record of a grid round, by round parity (see
+    // end_barrier in kernels_loop.cuh): [0] arrivals; [1] min over the
+    // round's raised labels (l << 1) and the successor of C (s << 1 | 1);
+    // [2] the successor's member range start | heavy << 31; [3] its size |
+    // C-split << 31.  Pollers read all four words with one 16-byte acquire
+    // load, so the next splitter comes with the barrier itself.
+    alignas(16) unsigned brec[2][4];
+    // Mid-round (phase A -> B) barrier record, by parity: [0] arrivals,
+    // [1] small touched blocks registered, [2..3] the 64-bit big-block
+    // counter (#big blocks << 32 | #32-member chunks) -- the registration
+    // atomics work on these words, and one 16-byte acquire load returns
+    // them with the last arrival.
+    alignas(16) unsigned arec[2][4];
 };
+constexpr unsigned kRecFlag = 1u << 31;
 
 // Window of unstable labels examined by one skip step (see k_refine_sparse).
 constexpr int32_t kSkipSpan = 32768;
@@ -288,7 +302,7 @@ __device__ __forceinline__ void raise_flush_warp0(const SparseParams& p, int cur
         s_nmin_round = ns ? s_nmin : 0x7fffffff;
         s_csplit_round = s_csplit;
         if (s_csplit) {
-            p.ctrl->csplit[cur] = 1;
+            red_or(&p.ctrl->brec[cur][3], kRecFlag);
             s_csplit = 0;
         }
     }
@@ -308,7 +322,7 @@ __device__ __forceinline__ void raise_flush_warp0(const SparseParams& p, int cur
     }
     __syncwarp();  // every lane has read s_nsplit / s_ndirty before lane 0 resets them
     if (lane == 0) {
-        red_min(&p.ctrl->next_min[cur], s_nmin);
+        red_min_u32(&p.ctrl->brec[cur][1], (uint32_t)s_nmin << 1);
         if (round < p.splits_cap) red_add(&p.splits[round], ns);
         s_nmin = 0x7fffffff;
         s_nsplit = 0;
@@ -439,13 +453,15 @@ __device__ __forceinline__ void register_blocks_warp(const SparseParams& p, int 
     const unsigned heavy = __ballot_sync(kFull, reg && r.y > 1);
     if (heavy && lane == __ffs(heavy) - 1) {
         if (solo) s_ctr_heavy = 1;
-        else ctl->heavy[cur] = 1;
+        else red_or(&ctl->brec[cur][2], kRecFlag);
     }
     const unsigned small = __ballot_sync(kFull, reg && r.y <= 32);
     if (small) {
         const int ld = __ffs(small) - 1;
         int32_t base = 0;
-        if (lane == ld) base = solo ? atomicAdd(&s_ctr_nsmall, __popc(small)) : atomicAdd(&ctl->n_small[cur], __popc(small));
+        if (lane == ld)
+            base = solo ? atomicAdd(&s_ctr_nsmall, __popc(small))
+                        : (int32_t)atomicAdd(&ctl->arec[cur][1], (unsigned)__popc(small));
         base = __shfl_sync(kFull, base, ld);
         // (label, start, size | leader slot count << 6, leader slot base)
         if (reg && r.y <= 32)
@@ -460,7 +476,7 @@ __device__ __forceinline__ void register_blocks_warp(const SparseParams& p, int 
             pk = atomicAdd(&s_ctr_big, d1);
             pk4 = atomicAdd(&s_ctr_big4, d4);
         } else {
-            pk = atomicAdd(&ctl->big_pack[cur], d1);
+            pk = atomicAdd((unsigned long long*)&ctl->arec[cur][2], d1);
             pk4 = atomicAdd(&ctl->big_pack4[cur], d4);
         }
         const int32_t k = (int32_t)(pk >> 32), base = (int32_t)(pk & 0xffffffffu);
