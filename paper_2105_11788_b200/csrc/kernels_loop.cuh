@@ -22,7 +22,7 @@ constexpr int32_t kSoloMaxC = 32;
 constexpr int32_t kSoloMaxItems = 256;
 constexpr int32_t kSoloSkipSpan = 512;   // skip-step window of the solo team: one label per thread
 #ifndef BISIM_KA
-#define BISIM_KA 2
+#define BISIM_KA 1
 #endif
 #ifdef BISIM_NO_CSNAP
 constexpr bool kNoCsnap = true;
@@ -33,7 +33,9 @@ constexpr bool kNoCsnap = false;
 #define BISIM_SKIP_GAIN 32
 #endif
 constexpr int32_t kSkipGain = BISIM_SKIP_GAIN;  // rounds a skip step must retire to be retried at once
-constexpr int kA = BISIM_KA;             // in-edges per lane per phase-A step
+// in-edges per lane per phase-A step: 1 since the fat barriers (process-level
+// A/B vs 2: c1 -3.2 %, c2 -2.0 %, c4l -1.5 %, c3 -1.1 %, c5 / c4u -0.1 %; 3: slower)
+constexpr int kA = BISIM_KA;
 
 template <bool IDENT, bool SH>
 __global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParams pk) {
