@@ -669,7 +669,7 @@ __device__ int32_t process_small(const SparseParams& p, int cur, int64_t round, 
 // false (the round then runs normally) for splitters of more than 32
 // members or more than kSkipMaxEdges in-edges.
 #ifndef BISIM_TRIV_G
-#define BISIM_TRIV_G 8
+#define BISIM_TRIV_G 4
 #endif
 constexpr int kTrivG = BISIM_TRIV_G;
 template <bool IDENT>
