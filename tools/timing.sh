@@ -8,5 +8,5 @@ try:
     d=json.loads(t)
 except Exception:
     print('$c', 'FAILED', t[-300:]); sys.exit()
-print('$c', 'ms=%.2f R=%d us/round=%.2f pre=%.2f label=%.2f alg=%.2f GB/s=%.1f ok=%s' % (d['ms_per_step'], d['config']['supersteps'], d['per_round_us'], d['phase_ms']['pre'], d['phase_ms']['label'], d['phase_ms']['alg'], d['roofline']['achieved'], d['config']['correct_vs_truth']))"
+print('$c', 'ms=%.2f R=%d us/round=%.2f pre=%.2f label=%.2f alg=%.2f GB/s=%.1f ok=%s' % (d['ms_per_step'], d['config']['supersteps'], d['per_round_us'], d['phase_ms']['pre'], d['phase_ms']['label'], d['phase_ms']['alg'], d['roofline']['achieved'], d.get('parity')))"
 done
