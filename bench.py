@@ -163,16 +163,18 @@ class CpuSampler:
     timed on a bounded sample of the workload.
 
     Setup -- preprocessing and the label pre-partition (BCRP) or pi0 (RCPP)
-    -- runs once and is timed once.  Main-loop rounds are timed in windows
-    of `window` rounds that start at the beginning, the middle and the end
-    of the run: the literal oracle resumes from the program state the
-    event-driven oracle reports after round r0 (oracle.fast_states, untimed
-    setup).  The estimate of one complete run is t_pre + t_label + R x
-    (mean of the windows' ms/round), with R the round count of the oracle's
-    own complete run (tests/golden/scale/).
+    -- runs once and is timed once.  Main-loop rounds are timed in `nwin`
+    windows of `window` rounds whose starts are spread evenly over the run
+    (first round to last): the literal oracle resumes from the program state
+    the event-driven oracle reports after round r0 (oracle.fast_states,
+    untimed setup).  Per-round cost varies along a run (c5: rounds 1-11 cost
+    ~2.5x the rounds of the second half, where the big blocks have already
+    split), so the windows are a stratified sample and the estimate of one
+    complete run is t_pre + t_label + R x (mean of the windows' ms/round),
+    R from the oracle's own complete run (tests/golden/scale/).
     """
 
-    def __init__(self, config: str, inst, window: int):
+    def __init__(self, config: str, inst, window: int, nwin: int):
         from oracle import oracle
         # all host threads, except where OpenMP fork/join per phase would
         # cost more than the phase (small systems run fastest on one core)
@@ -186,8 +188,10 @@ class CpuSampler:
         block0 = self.run.block()
         unstable0 = np.zeros(inst.n, np.uint8)
         unstable0[block0] = 1
-        starts = [0, self.R // 2, max(self.R - self.window, 0)]
-        later = sorted({r for r in starts if r > 0})
+        last = max(self.R - self.window, 0)
+        nwin = max(1, min(nwin, last + 1))
+        starts = sorted({(k * last) // max(nwin - 1, 1) for k in range(nwin)})
+        later = [r for r in starts if r > 0]
         states = oracle.fast_states(inst, later, threads=self.threads) if later else ([], [])
         by_round = {r: (states[0][i], states[1][i]) for i, r in enumerate(later)}
         by_round[0] = (block0, unstable0)
@@ -195,7 +199,7 @@ class CpuSampler:
         self.samples = {r: [] for r in starts}  # seconds per round, per window
 
     def step(self, i: int) -> float:
-        """Time one window (cycling start / middle / end); returns seconds."""
+        """Time one window (cycling through the windows); returns seconds."""
         r0, (block, unstable) = self.windows[i % len(self.windows)]
         self.run.set_state(block, unstable)
         k, sec = self.run.rounds(min(self.window, self.R - r0))
@@ -204,28 +208,29 @@ class CpuSampler:
         return sec
 
     def estimate(self):
-        per = [statistics.mean(v) for v in self.samples.values() if v]
-        per_round = statistics.mean(per)
+        per = {r: statistics.mean(v) for r, v in self.samples.items() if v}
+        per_round = statistics.mean(per.values())
         t = self.run.t_pre_s + self.run.t_label_s + self.R * per_round
         rounds = sum(len(v) for v in self.samples.values()) * self.window
+        ms = sorted(x * 1e3 for x in per.values())
         desc = (f"oracle port (oracle/bisim_oracle.c, literal O(n+m) rounds, OpenMP "
                 f"{self.threads} threads): setup (preprocessing + "
                 f"label pre-partition / pi0) timed once = {self.run.t_pre_s + self.run.t_label_s:.2f} s; "
-                f"{rounds} main-loop rounds timed in windows of {self.window} at rounds "
-                f"{', '.join(str(r + 1) for r, _ in self.windows)} of R = {self.R} "
-                f"({', '.join('%.3f' % (statistics.mean(v) * 1e3) for v in self.samples.values() if v)}"
-                f" ms/round); total extrapolated as t_setup + R x mean ms/round")
+                f"{rounds} main-loop rounds timed in {len(per)} windows of {self.window} rounds "
+                f"starting evenly from round 1 to {self.windows[-1][0] + 1} of R = {self.R} "
+                f"({ms[0]:.3f} .. {ms[-1]:.3f} ms/round, mean {per_round * 1e3:.3f}); "
+                f"total extrapolated as t_setup + R x mean ms/round")
         return t, per_round, desc
 
     def close(self):
         self.run.close()
 
 
-def cpu_baseline(config: str, inst, window: int = 70) -> dict:
-    """cpu_baseline of the GPU arm's line (rank 0, N=1): three windows."""
-    cs = CpuSampler(config, inst, window)
+def cpu_baseline(config: str, inst, window: int = 21, nwin: int = 10) -> dict:
+    """cpu_baseline of the GPU arm's line (rank 0, N=1): ten windows."""
+    cs = CpuSampler(config, inst, window, nwin)
     try:
-        for i in range(3):
+        for i in range(nwin):
             cs.step(i)
         t, per_round, desc = cs.estimate()
     finally:
@@ -243,15 +248,16 @@ def run_reference(args):
         return 0
     inst, desc = make_instance(args.config, 0)
     steps_total = args.warmup + args.steps
-    # >= 210 timed rounds over the K timed steps, windows cycling start/middle/end
+    # one window per timed step (up to 20), >= 210 timed rounds in total
+    nwin = max(2, min(args.steps, 20))
     window = max(10, -(-210 // max(args.steps, 1)))
-    cs = CpuSampler(args.config, inst, window)
+    cs = CpuSampler(args.config, inst, window, nwin)
     try:
         for i in range(steps_total):
             if i == args.warmup:
                 for v in cs.samples.values():
                     v.clear()
-            cs.step(i)
+            cs.step(i - args.warmup)  # timed step k runs window k
         t, per_round, sample = cs.estimate()
     finally:
         cs.close()
