@@ -40,6 +40,7 @@ __device__ __forceinline__ unsigned cluster_n() {
 // variant 0: flat counter (libbisim's grid_barrier)
 // variant 1: cluster barrier, rank-0 CTA arrives globally and spins, cluster barrier
 // variant 2: cluster barrier, rank-0 arrives, every CTA's thread 0 spins on the counter
+// variant 3: the first cluster alone syncs with the hardware cluster barrier (team = 1 cluster)
 __global__ void bench(Bar* b, int variant, int K, int work, unsigned* sink, unsigned long long* out) {
     unsigned gen = 0;
     const unsigned ncl = gridDim.x / (variant ? cluster_n() : 1u);
@@ -66,6 +67,9 @@ __global__ void bench(Bar* b, int variant, int K, int work, unsigned* sink, unsi
             }
             ++gen;
             cluster_sync_all();
+        } else if (variant == 3) {
+            // the cluster alone (a cluster-sized team): hardware cluster barrier only
+            if (blockIdx.x < cluster_n()) cluster_sync_all();
         } else {
             cluster_sync_all();
             if (threadIdx.x == 0) {
@@ -99,7 +103,7 @@ int main() {
     cudaFuncSetAttribute((void*)bench, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     for (int work : {0, 1}) {
         for (int cl : {1, 2, 4, 8, 16}) {
-            for (int v = 0; v < 3; ++v) {
+            for (int v = 0; v < 4; ++v) {
                 if ((cl == 1) != (v == 0)) continue;
                 // largest grid of whole clusters that is co-resident
                 cudaLaunchConfig_t cfg = {};
