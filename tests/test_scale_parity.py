@@ -123,3 +123,15 @@ def test_gpu_c5s_virtual_sharded_replicas():
                                         [0, 0], verify=True)
     _check(rec, block, st, ns, "c5s x2 sharded")
     assert np.array_equal(block, inst.truth)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", [1, 7])
+def test_gpu_c5_other_ranks_lifted_truth(seed):
+    """The instances ranks 1..7 refine in `bench.py --gpus N` (c5 seeds 1..7)
+    equal their lifted ground truth at full size."""
+    from paper_2105_11788_b200 import workloads as W
+    inst = W.c5_vlts(seed=seed)
+    block, st, _ = _run_gpu(inst)
+    assert np.array_equal(block, inst.truth)
+    assert st.final_block_count == len(np.unique(inst.truth))
