@@ -646,9 +646,11 @@ int run_with(Ctx& c, Job& j) {
 
     // ---- label pre-partition (bcrp.py:144-184) / pi0 (rcpp.py:58-72)
     if (j.bcrp && A > 0 && guard < A) {
+        // PramEngine.begin_superstep of label round guard+1 (pram.py:195-200)
         S.guard_count = std::max<int64_t>(guard + 1, 1);
         *j.st = S;
-        throw Error(BISIM_GUARD, "superstep guard exceeded during the label pre-partition");
+        throw Error(BISIM_GUARD, "superstep guard exceeded (" + std::to_string(S.guard_count) + " > " +
+                                     std::to_string(guard) + ")");
     }
     unsigned long long* nl = (unsigned long long*)c.nl.ensure((int64_t)n * 8);
     if (j.bcrp) {

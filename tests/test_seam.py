@@ -300,3 +300,24 @@ def test_reference_errors_for_bad_types():
         RelationInput(3, [(0, 3)], Partition([0, 0, 0]))
     with pytest.raises(TypeError):
         bcrp_run(_lts_pair(G.cases()["pre_fig2"])[0], object())
+
+
+def test_guard_messages_match_the_reference():
+    """SuperstepLimitError text is the reference's PramEngine message
+    `superstep guard exceeded (<step> > <max>)` (pram.py:195-200), for trips
+    in the label rounds and in the main loop."""
+    for g in G.cases()["guard"]:
+        if not g["result"]["guard"]:
+            continue
+        rec = G.cases()[g["instance"]]
+        lts, _ = _lts_pair(rec)
+        with pytest.raises(SuperstepLimitError) as e:
+            if g["kind"] == "bcrp":
+                bcrp_run(lts, Priority(), max_supersteps=g["max_supersteps"])
+            else:
+                n = rec["n"]
+                rcpp_run(RelationInput(n, list(zip(rec["src"], rec["dst"])), Partition([0] * n)),
+                         Priority(), max_supersteps=g["max_supersteps"])
+        msg = str(e.value)
+        assert msg.startswith("superstep guard exceeded (") and msg.endswith(
+            f" > {g['max_supersteps']})"), msg
