@@ -194,13 +194,17 @@ def test_gpu_post_vs_oracle_medium(seed):
 
 
 @pytest.mark.gpu
-def test_gpu_coarsest_partition_is_stable_at_scale():
-    """The refinement result of a lifted c4-shaped system is stable, and its
-    quotient has exactly one state per block (size-independent properties)."""
+@pytest.mark.parametrize("size", ["small", "full_c5"])
+def test_gpu_coarsest_partition_is_stable(size):
+    """The refinement result is stable, its quotient has exactly one state per
+    block, and merging two blocks breaks stability (size-independent
+    properties) -- on a small lifted system and on config c5 at full size
+    (n=10M, m=100M)."""
     from paper_2105_11788_b200 import bcrp_arrays
     from paper_2105_11788_b200 import workloads as W
     from paper_2105_11788_b200.post import is_stable_arrays, quotient_arrays
-    inst = W.lifted_quotient(3000, 200, 64, 4, 2, 2, seed=5)
+    inst = (W.lifted_quotient(3000, 200, 64, 4, 2, 2, seed=5) if size == "small"
+            else W.c5_vlts(seed=0))
     block, st, _ = bcrp_arrays(inst.n, inst.src, inst.act, inst.dst, inst.num_actions)
     assert np.array_equal(block, inst.truth)
     assert is_stable_arrays(inst.n, inst.src, inst.act, inst.dst, inst.num_actions, block)
