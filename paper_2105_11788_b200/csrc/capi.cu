@@ -76,6 +76,8 @@ struct Ctx {
         lmins, sarr, big_list4, big_base4, big_info, big_info4, sinfo, nrm, bcur, stage;
     int launches = 0;
     struct Stager* stager = nullptr;  // pinned staging of pageable host arrays (lazy)
+    cudaStream_t cstream = nullptr;   // host-to-device copies overlapping preprocessing
+    std::vector<cudaEvent_t> pev;     // their events (lazy)
     ~Ctx();
 };
 
@@ -112,6 +114,7 @@ std::unique_ptr<Ctx> make_ctx(int device) {
         if (!prop.cooperativeLaunch) throw Error(BISIM_CUDA, "device lacks cooperative launch");
         c->sms = prop.multiProcessorCount;
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
         for (auto& e : c->ev) CK(cudaEventCreate(&e));
         c->grid_refine_bcrp = occupancy_grid((const void*)k_refine<false>, c->sms);
         c->grid_refine_rcpp = occupancy_grid((const void*)k_refine<true>, c->sms);
@@ -172,6 +175,8 @@ Ctx::~Ctx() {
     }
     for (auto& e : ev)
         if (e) cudaEventDestroy(e);
+    for (auto e : pev) cudaEventDestroy(e);
+    if (cstream) cudaStreamDestroy(cstream);
     if (stream) cudaStreamDestroy(stream);
 }
 
@@ -462,35 +467,16 @@ LabelTables label_tables(Ctx& c, int32_t n, int64_t m, int32_t A, const int32_t*
     return t;
 }
 
-// Reverse CSR fill (sparse modes): bucketed staging pass + in-order placement
-// (kernels_sparse.cuh k_rev_bucket / k_rev_place).  cursor = copy of rev_ptr.
-template <bool BCRP>
-void rev_fill_bucketed(Ctx& c, int32_t n, int64_t m, const int32_t* d_src, const int32_t* d_act,
-                       const int32_t* d_dst, const unsigned long long* lmask, const int32_t* off,
-                       const int4* sinfo, const int32_t* rev_ptr, int32_t* cursor, int2* rev2, int32_t* rev_src,
-                       int32_t src_lo, int32_t src_hi) {
-    cudaStream_t st = c.stream;
-    int shift = 0;
-    while (((int64_t)n >> shift) >= 256) ++shift;  // <= 256 buckets
-    const int32_t nb = (int32_t)(((int64_t)n - 1) >> shift) + 1;
-    int32_t* bcur = (int32_t*)c.bcur.ensure((int64_t)nb * 4);
-    int4* stage = (int4*)c.stage.ensure(std::max<int64_t>(m, 1) * 16);
-    k_bucket_init<<<(nb + 255) / 256, 256, 0, st>>>(n, shift, nb, rev_ptr, bcur);
-    const int64_t tiles = (m + kBucketTile - 1) / kBucketTile;
-    const int g1 = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)c.sms * 4));
-    k_rev_bucket<BCRP><<<g1, kBucketThreads, 0, st>>>(n, m, d_src, d_act, d_dst, lmask, off, sinfo, shift, nb, bcur,
-                                                      stage, src_lo, src_hi);
-    // staged in-edges: rev_ptr[n] <= m of them (only sources in [src_lo, src_hi)).
-    // Exactly the resident number of CTAs: the grid-stride sweep then moves
-    // through the staging array as one wave, so the rev positions being
-    // written stay within a few MB (an oversubscribed grid sweeps twice,
-    // half a window each time, and the sectors leave L2 half-written).
-    int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k_rev_place<BCRP>, 256, 0));
-    const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c.sms * std::max(occ, 1), (m + 255) / 256));
-    k_rev_place<BCRP><<<g2, 256, 0, st>>>(rev_ptr + n, stage, cursor, rev2, rev_src);
-    c.launches += 3;
-    CK(cudaGetLastError());
+// Host-input pipelining of large labelled systems (run_with): chunks of the
+// src / act copies overlap the per-transition passes.
+constexpr int64_t kPipeMin = 1 << 22;
+constexpr int kPipeChunks = 8;
+cudaEvent_t* pipe_events(Ctx& c) {
+    if (c.pev.empty()) {
+        c.pev.resize(kPipeChunks + 2);
+        for (auto& e : c.pev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    return c.pev.data();
 }
 
 int run_with(Ctx& c, Job& j);
@@ -526,34 +512,8 @@ int run_with(Ctx& c, Job& j) {
     S.label_rounds = A;
     S.mode = stepped ? BISIM_MODE_STEPPED : (dense ? BISIM_MODE_DENSE : BISIM_MODE_PERSISTENT);
 
-    // ---- inputs
-    const int64_t mm = std::max<int64_t>(m, 1);
-    const int32_t* d_src;
-    const int32_t* d_act = nullptr;
-    const int32_t* d_dst;
-    const int32_t* d_pi0 = nullptr;
-    CK(cudaEventRecord(c.ev[0], st));
-    if (j.inputs_on_device) {
-        d_src = j.src;
-        d_act = j.act;
-        d_dst = j.dst;
-        d_pi0 = j.pi0;
-    } else {
-        d_src = (int32_t*)c.src.ensure(mm * 4);
-        d_dst = (int32_t*)c.dst.ensure(mm * 4);
-        h2d(c, (void*)d_src, j.src, m * 4, st);
-        h2d(c, (void*)d_dst, j.dst, m * 4, st);
-        if (j.bcrp) {
-            d_act = (int32_t*)c.act.ensure(mm * 4);
-            h2d(c, (void*)d_act, j.act, m * 4, st);
-        } else {
-            d_pi0 = (int32_t*)c.pi0.ensure((int64_t)n * 4);
-            h2d(c, (void*)d_pi0, j.pi0, (int64_t)n * 4, st);
-        }
-    }
-    CK(cudaEventRecord(c.ev[1], st));
-
     // ---- buffers
+    const int64_t mm = std::max<int64_t>(m, 1);
     Ctrl* ctrl = (Ctrl*)c.ctrl.ensure(std::max(sizeof(Ctrl), sizeof(SCtrl)));
     unsigned long long* lmask =
         j.bcrp ? (unsigned long long*)c.lmask.ensure((size_t)std::max(W, 1) * n * 8) : nullptr;
@@ -570,29 +530,117 @@ int run_with(Ctx& c, Job& j) {
     const int64_t splits_dev_cap =
         std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(guard - A, 1), 3LL * n + 16));
     int32_t* splits = (int32_t*)c.splits.ensure(splits_dev_cap * 4);
+    int32_t* rev_slot = nullptr;  // dense: slot per in-edge
+    int2* rev2 = nullptr;         // sparse BCRP: (slot, source)
+    int32_t* rev_src = nullptr;   // sparse RCPP: source
+    if (dense) rev_slot = (int32_t*)c.rev_slot.ensure(mm * 4);
+    else if (j.bcrp) rev2 = (int2*)c.rev2.ensure(mm * 8);
+    else rev_src = (int32_t*)c.rev_slot.ensure(mm * 4);
+    // sparse modes: reverse CSR through the bucketed staging array
+    // (kernels_sparse.cuh k_rev_bucket / k_rev_place), <= 256 target buckets
+    int shift = 0;
+    while (((int64_t)n >> shift) >= 256) ++shift;
+    const int32_t nb = (int32_t)(((int64_t)n - 1) >> shift) + 1;
+    int32_t* bcur = dense ? nullptr : (int32_t*)c.bcur.ensure((int64_t)nb * 4);
+    int4* stage = dense ? nullptr : (int4*)c.stage.ensure(mm * 16);
+    auto bucket_pass = [&](int64_t len, const int32_t* s_, const int32_t* a_, const int32_t* d_, int32_t lo,
+                           int32_t hi, const int4* si) {
+        if (len <= 0) return;
+        const int64_t tiles = (len + kBucketTile - 1) / kBucketTile;
+        const int g1 = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)c.sms * 4));
+        k_rev_bucket<<<g1, kBucketThreads, 0, st>>>(len, s_, a_, d_, shift, nb, bcur, stage, lo, hi, si);
+        ++c.launches;
+    };
+    auto rev_ptr_scan = [&]() {
+        scan_excl(c, rev_ptr, n);
+        CK(cudaMemcpyAsync(cursor, rev_ptr, ((int64_t)n + 1) * 4, cudaMemcpyDeviceToDevice, st));
+        if (!dense) {
+            k_bucket_init<<<(nb + 255) / 256, 256, 0, st>>>(n, shift, nb, rev_ptr, bcur);
+            ++c.launches;
+        }
+    };
 
+    // ---- inputs + preprocessing (bcrp.py:49-126)
     const int TB = 256;
-    // ---- preprocessing (bcrp.py:49-126)
+    const int32_t* d_src;
+    const int32_t* d_act = nullptr;
+    const int32_t* d_dst;
+    const int32_t* d_pi0 = nullptr;
+    // A large labelled system from host memory: the copies of src / act
+    // overlap the per-transition passes (label sets, target buckets) of the
+    // chunks already on the device; dst goes first, its in-degrees fix the
+    // bucket layout.
+    const bool pipe = j.bcrp && !j.inputs_on_device && !sharded && !dense && m >= kPipeMin;
+    CK(cudaEventRecord(c.ev[0], st));
     CK(cudaMemsetAsync(ctrl, 0, std::max(sizeof(Ctrl), sizeof(SCtrl)), st));
-    if (j.bcrp) {
-        CK(cudaMemsetAsync(lmask, 0, (size_t)std::max(W, 1) * n * 8, st));
-        if (m) {
-            k_label_mask<<<grid_for(m, TB, c.sms), TB, 0, st>>>(n, m, A, d_src, d_act, d_dst, lmask, ctrl);
-            ++c.launches;
-        }
-        k_nr_marks<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, W, lmask, off);
+    CK(cudaMemsetAsync(rev_ptr, 0, ((int64_t)n + 1) * 4, st));
+    if (j.bcrp) CK(cudaMemsetAsync(lmask, 0, (size_t)std::max(W, 1) * n * 8, st));
+    if (pipe) {
+        int32_t* ds = (int32_t*)c.src.ensure(mm * 4);
+        int32_t* dd = (int32_t*)c.dst.ensure(mm * 4);
+        int32_t* da = (int32_t*)c.act.ensure(mm * 4);
+        d_src = ds;
+        d_dst = dd;
+        d_act = da;
+        cudaStream_t cs = c.cstream;
+        cudaEvent_t* pev = pipe_events(c);
+        CK(cudaEventRecord(pev[0], st));  // the buffers' previous readers are done
+        CK(cudaStreamWaitEvent(cs, pev[0], 0));
+        h2d(c, dd, j.dst, m * 4, cs);
+        CK(cudaEventRecord(pev[1], cs));
+        CK(cudaStreamWaitEvent(st, pev[1], 0));
+        CK(cudaEventRecord(c.ev[1], st));
+        k_indeg_checked<<<grid_for(m, TB, c.sms), TB, 0, st>>>(n, m, dd, rev_ptr, ctrl);
         ++c.launches;
-        scan_excl(c, off, n);
+        rev_ptr_scan();
+        const int64_t chunk = (m + kPipeChunks - 1) / kPipeChunks;
+        for (int k = 0; k < kPipeChunks; ++k) {
+            const int64_t i0 = k * chunk, len = std::min<int64_t>(chunk, m - i0);
+            if (len <= 0) break;
+            h2d(c, ds + i0, j.src + i0, len * 4, cs);
+            h2d(c, da + i0, j.act + i0, len * 4, cs);
+            CK(cudaEventRecord(pev[2 + k], cs));
+            CK(cudaStreamWaitEvent(st, pev[2 + k], 0));
+            k_label_mask<<<grid_for(len, TB, c.sms), TB, 0, st>>>(n, len, A, ds + i0, da + i0, dd + i0, lmask, ctrl);
+            ++c.launches;
+            bucket_pass(len, ds + i0, da + i0, dd + i0, 0, n, nullptr);  // (t, s, action)
+        }
     } else {
-        if (m) {
-            k_check_edges<<<grid_for(m, TB, c.sms), TB, 0, st>>>(n, m, d_src, d_dst, ctrl);
+        if (j.inputs_on_device) {
+            d_src = j.src;
+            d_act = j.act;
+            d_dst = j.dst;
+            d_pi0 = j.pi0;
+        } else {
+            d_src = (int32_t*)c.src.ensure(mm * 4);
+            d_dst = (int32_t*)c.dst.ensure(mm * 4);
+            h2d(c, (void*)d_src, j.src, m * 4, st);
+            h2d(c, (void*)d_dst, j.dst, m * 4, st);
+            if (j.bcrp) {
+                d_act = (int32_t*)c.act.ensure(mm * 4);
+                h2d(c, (void*)d_act, j.act, m * 4, st);
+            } else {
+                d_pi0 = (int32_t*)c.pi0.ensure((int64_t)n * 4);
+                h2d(c, (void*)d_pi0, j.pi0, (int64_t)n * 4, st);
+            }
+        }
+        CK(cudaEventRecord(c.ev[1], st));
+        if (j.bcrp) {
+            if (m) {
+                k_label_mask<<<grid_for(m, TB, c.sms), TB, 0, st>>>(n, m, A, d_src, d_act, d_dst, lmask, ctrl);
+                ++c.launches;
+            }
+        } else {
+            if (m) {
+                k_check_edges<<<grid_for(m, TB, c.sms), TB, 0, st>>>(n, m, d_src, d_dst, ctrl);
+                ++c.launches;
+            }
+            k_check_pi0<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, d_pi0, ctrl);
             ++c.launches;
         }
-        k_check_pi0<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, d_pi0, ctrl);
-        ++c.launches;
     }
-    // Validation must finish before anything scatters through src/dst
-    // (k_indeg, the reverse fill): read the flag back here.
+    // Validation must finish before anything indexes by a source or action
+    // (in-degrees, slots, the reverse fill): read the flag back here.
     {
         int32_t bad = 0;
         CK(cudaGetLastError());
@@ -602,38 +650,56 @@ int run_with(Ctx& c, Job& j) {
             throw Error(BISIM_BAD_INPUT, j.bcrp ? "transition mentions a state or action outside range"
                                                 : "edge outside 0..n-1 or pi0 is not a leader-form partition");
     }
-    CK(cudaMemsetAsync(rev_ptr, 0, ((int64_t)n + 1) * 4, st));
-    if (m) {
-        k_indeg<<<grid_for(m, TB, c.sms), TB, 0, st>>>(m, d_dst, rev_ptr, sharded ? d_src : nullptr, src_lo,
-                                                       src_hi);
+    int4* sinfo = nullptr;
+    if (j.bcrp) {
+        k_nr_marks<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, W, lmask, off);
         ++c.launches;
+        scan_excl(c, off, n);
+        if (W == 1 && !dense) {
+            sinfo = (int4*)c.sinfo.ensure((int64_t)n * 16);
+            k_pack_sinfo<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, lmask, off, sinfo);
+            ++c.launches;
+        }
     }
-    scan_excl(c, rev_ptr, n);
-    CK(cudaMemcpyAsync(cursor, rev_ptr, ((int64_t)n + 1) * 4, cudaMemcpyDeviceToDevice, st));
-    int32_t* rev_slot = nullptr;  // dense: slot per in-edge
-    int2* rev2 = nullptr;         // sparse BCRP: (slot, source)
-    int32_t* rev_src = nullptr;   // sparse RCPP: source
-    if (dense) rev_slot = (int32_t*)c.rev_slot.ensure(mm * 4);
-    else if (j.bcrp) rev2 = (int2*)c.rev2.ensure(mm * 8);
-    else rev_src = (int32_t*)c.rev_slot.ensure(mm * 4);
+    // the mark slot goes into the staging array in pass 1 when the label
+    // sets are already complete (every path but the pipelined one)
+    const bool slot_staged = !pipe && sinfo != nullptr;
+    if (!pipe) {
+        if (m) {
+            k_indeg<<<grid_for(m, TB, c.sms), TB, 0, st>>>(m, d_dst, rev_ptr, sharded ? d_src : nullptr, src_lo,
+                                                           src_hi);
+            ++c.launches;
+        }
+        rev_ptr_scan();
+        if (!dense) bucket_pass(m, d_src, d_act, d_dst, src_lo, src_hi, slot_staged ? sinfo : nullptr);
+    }
     if (m) {
-        const int g = grid_for(m, TB, c.sms);
-        if (dense && j.bcrp)
-            k_rev_fill<true><<<g, TB, 0, st>>>(n, m, d_src, d_act, d_dst, lmask, off, cursor, rev_slot);
-        else if (dense)
-            k_rev_fill<false><<<g, TB, 0, st>>>(n, m, d_src, d_act, d_dst, lmask, off, cursor, rev_slot);
-        else if (j.bcrp) {
-            int4* sinfo = nullptr;
-            if (W == 1) {
-                sinfo = (int4*)c.sinfo.ensure((int64_t)n * 16);
-                k_pack_sinfo<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, lmask, off, sinfo);
-                ++c.launches;
-            }
-            rev_fill_bucketed<true>(c, n, m, d_src, d_act, d_dst, lmask, off, sinfo, rev_ptr, cursor, rev2, nullptr,
-                                    src_lo, src_hi);
+        if (dense) {
+            const int g = grid_for(m, TB, c.sms);
+            if (j.bcrp) k_rev_fill<true><<<g, TB, 0, st>>>(n, m, d_src, d_act, d_dst, lmask, off, cursor, rev_slot);
+            else k_rev_fill<false><<<g, TB, 0, st>>>(n, m, d_src, d_act, d_dst, lmask, off, cursor, rev_slot);
         } else {
-            rev_fill_bucketed<false>(c, n, m, d_src, d_act, d_dst, lmask, off, nullptr, rev_ptr, cursor, nullptr,
-                                     rev_src, src_lo, src_hi);
+            // exactly the resident number of CTAs: the grid-stride sweep then
+            // moves through the staging array as one wave, so the positions
+            // being written stay within a few MB (an oversubscribed grid
+            // sweeps twice, half a window each, and sectors leave L2
+            // half-written)
+            const void* fn = !j.bcrp    ? (const void*)k_rev_place<false, false>
+                             : slot_staged ? (const void*)k_rev_place<true, true>
+                                           : (const void*)k_rev_place<true, false>;
+            int occ = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, 0));
+            const int g2 =
+                (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c.sms * std::max(occ, 1), (m + 255) / 256));
+            if (!j.bcrp)
+                k_rev_place<false, false><<<g2, 256, 0, st>>>(rev_ptr + n, stage, cursor, nullptr, rev_src, n, nullptr,
+                                                              nullptr, nullptr);
+            else if (slot_staged)
+                k_rev_place<true, true><<<g2, 256, 0, st>>>(rev_ptr + n, stage, cursor, rev2, nullptr, n, lmask, off,
+                                                            sinfo);
+            else
+                k_rev_place<true, false><<<g2, 256, 0, st>>>(rev_ptr + n, stage, cursor, rev2, nullptr, n, lmask,
+                                                             off, sinfo);
         }
         ++c.launches;
     }

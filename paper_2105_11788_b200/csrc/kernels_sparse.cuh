@@ -834,39 +834,45 @@ __global__ void k_bucket_init(int32_t n, int shift, int32_t nb, const int32_t* _
         bcur[b] = rev_ptr[min((int64_t)b << shift, (int64_t)n)];
 }
 
-template <bool BCRP>
+// Pass 1 over transitions [0, m) of (src, act, dst) -- a chunk of the input
+// (the host path runs it per chunk while the next chunk is still being
+// copied): stage (target, source, action) by target bucket.  Targets were
+// validated before (k_indeg_checked); sources and actions may still be out
+// of range, which the caller detects (k_label_mask) before pass 2 uses them.
+//
+// sinfo != nullptr (the label sets are complete, |Act| <= 64): the mark slot
+// is computed here instead of the action, so pass 2 needs no per-source
+// lookup (the device-resident path: the random sinfo read overlaps the
+// tile's other loads better here).
 __global__ void __launch_bounds__(kBucketThreads) k_rev_bucket(
-    int32_t n, int64_t m, const int32_t* __restrict__ src, const int32_t* __restrict__ act,
-    const int32_t* __restrict__ dst, const unsigned long long* __restrict__ lmask,
-    const int32_t* __restrict__ off, const int4* __restrict__ sinfo, int shift, int32_t nb, int32_t* bcur,
-    int4* stage, int32_t lo, int32_t hi) {
+    int64_t m, const int32_t* __restrict__ src, const int32_t* __restrict__ act,
+    const int32_t* __restrict__ dst, int shift, int32_t nb, int32_t* bcur, int4* stage, int32_t lo, int32_t hi,
+    const int4* __restrict__ sinfo = nullptr) {
     __shared__ int32_t cnt[kMaxBuckets];
     __shared__ int32_t base[kMaxBuckets];
     for (int64_t t0 = (int64_t)blockIdx.x * kBucketTile; t0 < m; t0 += (int64_t)gridDim.x * kBucketTile) {
         for (int b = threadIdx.x; b < nb; b += blockDim.x) cnt[b] = 0;
         __syncthreads();
-        int32_t t[kBucketItems], slot[kBucketItems], s[kBucketItems], r[kBucketItems];
+        int32_t t[kBucketItems], s[kBucketItems], a[kBucketItems], r[kBucketItems];
 #pragma unroll
         for (int k = 0; k < kBucketItems; ++k) {
             const int64_t i = t0 + k * kBucketThreads + threadIdx.x;
             t[k] = -1;
             if (i < m) {
                 s[k] = src[i];
-                if (s[k] >= lo && s[k] < hi) t[k] = dst[i];
+                if (s[k] >= lo && s[k] < hi) {
+                    t[k] = dst[i];
+                    a[k] = act ? act[i] : 0;
+                }
             }
         }
 #pragma unroll
         for (int k = 0; k < kBucketItems; ++k) {
             if (t[k] < 0) continue;
-            const int64_t i = t0 + k * kBucketThreads + threadIdx.x;
-            if (!BCRP) {
-                slot[k] = s[k];
-            } else if (sinfo) {
+            if (sinfo) {  // a[k] := the mark slot
                 const int4 q = sinfo[s[k]];
                 const unsigned long long w = ((unsigned long long)(uint32_t)q.y << 32) | (uint32_t)q.x;
-                slot[k] = q.z + __popcll(w & ((1ull << (act[i] & 63)) - 1ull));
-            } else {
-                slot[k] = off[s[k]] + label_rank(lmask, n, s[k], act[i]);
+                a[k] = q.z + __popcll(w & ((1ull << (a[k] & 63)) - 1ull));
             }
             r[k] = atomicAdd(&cnt[t[k] >> shift], 1);
         }
@@ -876,14 +882,41 @@ __global__ void __launch_bounds__(kBucketThreads) k_rev_bucket(
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < kBucketItems; ++k)
-            if (t[k] >= 0) stage[base[t[k] >> shift] + r[k]] = make_int4(t[k], slot[k], s[k], 0);
+            if (t[k] >= 0) stage[base[t[k] >> shift] + r[k]] = make_int4(t[k], s[k], a[k], 0);
         __syncthreads();
     }
 }
 
-template <bool BCRP>
+// In-degree histogram of the targets in range; an out-of-range target flags
+// the input as bad and is not counted (nothing is scattered through it).
+__global__ void k_indeg_checked(int32_t n, int64_t m, const int32_t* __restrict__ dst, int32_t* cnt, Ctrl* ctrl) {
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < m; i0 += stride) {
+        const int64_t i = i0 + lane;
+        bool in = false;
+        int32_t t = -1 - lane;
+        if (i < m) {
+            t = dst[i];
+            in = (unsigned)t < (unsigned)n;
+            if (!in) {
+                ctrl->bad = 1;
+                t = -1 - lane;
+            }
+        }
+        const LaneRun r = lane_run(t);
+        if (in && r.rank == 0) red_add(&cnt[t], r.len);
+    }
+}
+
+// Pass 2: in staging order, each in-edge takes the next position of its
+// target; BCRP computes its mark slot off[s] + rank of the action among s's
+// labels (bcrp.py:219) here, once every label set is known.
+// SLOT: pass 1 already put the mark slot in the action's place.
+template <bool BCRP, bool SLOT>
 __global__ void k_rev_place(const int32_t* __restrict__ ptotal, const int4* __restrict__ stage, int32_t* cursor,
-                            int2* rev, int32_t* rev_src) {
+                            int2* rev, int32_t* rev_src, int32_t n, const unsigned long long* __restrict__ lmask,
+                            const int32_t* __restrict__ off, const int4* __restrict__ sinfo) {
     const int lane = threadIdx.x & 31;
     const int64_t total = *ptotal;
     for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < total;
@@ -896,8 +929,22 @@ __global__ void k_rev_place(const int32_t* __restrict__ ptotal, const int4* __re
         if (i < total && run.rank == 0) at = atomicAdd(&cursor[q.x], run.len);
         at = __shfl_sync(kFull, at, run.leader) + run.rank;
         if (i < total) {
-            if (BCRP) rev[at] = make_int2(q.y, q.z);
-            else rev_src[at] = q.z;
+            if (BCRP) {
+                const int32_t sv = q.y, a = q.z;
+                int32_t slot;
+                if (SLOT) {
+                    slot = a;
+                } else if (sinfo) {
+                    const int4 si = sinfo[sv];
+                    const unsigned long long w = ((unsigned long long)(uint32_t)si.y << 32) | (uint32_t)si.x;
+                    slot = si.z + __popcll(w & ((1ull << (a & 63)) - 1ull));
+                } else {
+                    slot = off[sv] + label_rank(lmask, n, sv, a);
+                }
+                rev[at] = make_int2(slot, sv);
+            } else {
+                rev_src[at] = q.y;
+            }
         }
     }
 }
