@@ -120,8 +120,8 @@ std::unique_ptr<Ctx> make_ctx(int device) {
         c->grid_refine_rcpp = occupancy_grid((const void*)k_refine<true>, c->sms);
         c->grid_label = occupancy_grid((const void*)k_label_rounds, c->sms);
         c->grid_label_common = occupancy_grid((const void*)k_label_rounds_common, c->sms);
-        c->grid_sparse_bcrp = occupancy_grid((const void*)k_refine_sparse<false, false>, c->sms, kSparseThreads, 1);
-        c->grid_sparse_rcpp = occupancy_grid((const void*)k_refine_sparse<true, false>, c->sms, kSparseThreads, 1);
+        c->grid_sparse_bcrp = occupancy_grid((const void*)k_refine_sparse<false, false>, c->sms, kSparseThreads, kSparsePerSm);
+        c->grid_sparse_rcpp = occupancy_grid((const void*)k_refine_sparse<true, false>, c->sms, kSparseThreads, kSparsePerSm);
         return c;
     }
 }

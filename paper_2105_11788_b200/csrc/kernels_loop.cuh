@@ -38,7 +38,7 @@ constexpr int32_t kSkipGain = BISIM_SKIP_GAIN;  // rounds a skip step must retir
 constexpr int kA = BISIM_KA;
 
 template <bool IDENT, bool SH>
-__global__ void __launch_bounds__(kSparseThreads, 1) k_refine_sparse(SparseParams pk) {
+__global__ void __launch_bounds__(kSparseThreads, kSparsePerSm) k_refine_sparse(SparseParams pk) {
     // SH (transition-sharded replica, kernels_shard.cuh): the round-parity
     // buffers are selected per round on a local copy of the parameters;
     // otherwise p is the kernel parameter itself

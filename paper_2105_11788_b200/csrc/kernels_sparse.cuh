@@ -36,6 +36,10 @@ namespace bisim {
 #define BISIM_SPARSE_THREADS 512
 #endif
 constexpr int kSparseThreads = BISIM_SPARSE_THREADS;
+#ifndef BISIM_SPARSE_PER_SM
+#define BISIM_SPARSE_PER_SM 1
+#endif
+constexpr int kSparsePerSm = BISIM_SPARSE_PER_SM;  // persistent CTAs per SM
 constexpr int kMaxShards = 8;         // replicas of the transition-sharded mode
 
 // Grid barrier: one monotonic arrival counter; CTA leaders add with
