@@ -321,3 +321,23 @@ def test_guard_messages_match_the_reference():
         msg = str(e.value)
         assert msg.startswith("superstep guard exceeded (") and msg.endswith(
             f" > {g['max_supersteps']})"), msg
+
+
+@pytest.mark.parametrize("name", ["pre_fig2", "pre_no_outgoing", "pre_stable_sort", "fanout_17"])
+def test_c_abi_preprocess_per_original_transition(name):
+    """bisim_preprocess (include/bisim.h): order per ORIGINAL transition,
+    nr_marks and off per state -- the reference's tables (bcrp.py:91-113)
+    read through the stable sort's permutation."""
+    import ctypes
+    rec = G.cases()[name]
+    n, src, act, dst, A = G.arrays(rec)
+    m = src.size
+    order = np.empty(max(m, 1), np.int32)
+    nr = np.empty(n, np.int32)
+    off = np.empty(n, np.int32)
+    L = ctypes.c_int64(0)
+    N.check(N.lib().bisim_preprocess(n, m, A, N.ptr(src), N.ptr(act), N.ptr(order), N.ptr(nr),
+                                     N.ptr(off), ctypes.byref(L), 0))
+    perm, sw, ref_order, ref_nr, ref_off, ref_L = oracle.preprocess(n, src, act, A)
+    assert list(order[:m][perm]) == list(ref_order)
+    assert list(nr) == list(ref_nr) and list(off) == list(ref_off) and L.value == ref_L
