@@ -149,6 +149,7 @@ Stager& stager(Ctx& c) {
     auto* S = new Stager();
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
     S->T = (int)std::max(1u, std::min(8u, hw / 2));
+    if (const char* e = getenv("BISIM_DEV") ? getenv("BISIM_STAGE_THREADS") : nullptr) S->T = std::max(1, atoi(e));
     S->buf.resize(2 * S->T);
     S->streams.resize(S->T);
     S->done.resize(2 * S->T);
