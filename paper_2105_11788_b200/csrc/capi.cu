@@ -545,11 +545,12 @@ int run_with(Ctx& c, Job& j) {
     int32_t* bcur = dense ? nullptr : (int32_t*)c.bcur.ensure((int64_t)nb * 4);
     int4* stage = dense ? nullptr : (int4*)c.stage.ensure(mm * 16);
     auto bucket_pass = [&](int64_t len, const int32_t* s_, const int32_t* a_, const int32_t* d_, int32_t lo,
-                           int32_t hi, const int4* si) {
+                           int32_t hi, bool slot_here, const int4* si) {
         if (len <= 0) return;
         const int64_t tiles = (len + kBucketTile - 1) / kBucketTile;
         const int g1 = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)c.sms * 4));
-        k_rev_bucket<<<g1, kBucketThreads, 0, st>>>(len, s_, a_, d_, shift, nb, bcur, stage, lo, hi, si);
+        k_rev_bucket<<<g1, kBucketThreads, 0, st>>>(len, s_, a_, d_, shift, nb, bcur, stage, lo, hi, slot_here, n,
+                                                    si, lmask, off);
         ++c.launches;
     };
     auto rev_ptr_scan = [&]() {
@@ -604,7 +605,7 @@ int run_with(Ctx& c, Job& j) {
             CK(cudaStreamWaitEvent(st, pev[2 + k], 0));
             k_label_mask<<<grid_for(len, TB, c.sms), TB, 0, st>>>(n, len, A, ds + i0, da + i0, dd + i0, lmask, ctrl);
             ++c.launches;
-            bucket_pass(len, ds + i0, da + i0, dd + i0, 0, n, nullptr);  // (t, s, action)
+            bucket_pass(len, ds + i0, da + i0, dd + i0, 0, n, false, nullptr);  // (t, s, action)
         }
     } else {
         if (j.inputs_on_device) {
@@ -664,7 +665,7 @@ int run_with(Ctx& c, Job& j) {
     }
     // the mark slot goes into the staging array in pass 1 when the label
     // sets are already complete (every path but the pipelined one)
-    const bool slot_staged = !pipe && sinfo != nullptr;
+    const bool slot_staged = !pipe && j.bcrp;
     if (!pipe) {
         if (m) {
             k_indeg<<<grid_for(m, TB, c.sms), TB, 0, st>>>(m, d_dst, rev_ptr, sharded ? d_src : nullptr, src_lo,
@@ -672,7 +673,7 @@ int run_with(Ctx& c, Job& j) {
             ++c.launches;
         }
         rev_ptr_scan();
-        if (!dense) bucket_pass(m, d_src, d_act, d_dst, src_lo, src_hi, slot_staged ? sinfo : nullptr);
+        if (!dense) bucket_pass(m, d_src, d_act, d_dst, src_lo, src_hi, slot_staged, sinfo);
     }
     if (m) {
         if (dense) {

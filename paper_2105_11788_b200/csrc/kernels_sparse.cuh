@@ -844,14 +844,14 @@ __global__ void k_bucket_init(int32_t n, int shift, int32_t nb, const int32_t* _
 // validated before (k_indeg_checked); sources and actions may still be out
 // of range, which the caller detects (k_label_mask) before pass 2 uses them.
 //
-// sinfo != nullptr (the label sets are complete, |Act| <= 64): the mark slot
-// is computed here instead of the action, so pass 2 needs no per-source
-// lookup (the device-resident path: the random sinfo read overlaps the
-// tile's other loads better here).
+// slot_here (the label sets are complete): the mark slot is computed here
+// instead of the action, so pass 2 needs no per-source lookup (the random
+// label-set read overlaps the tile's other loads better here).
 __global__ void __launch_bounds__(kBucketThreads) k_rev_bucket(
     int64_t m, const int32_t* __restrict__ src, const int32_t* __restrict__ act,
     const int32_t* __restrict__ dst, int shift, int32_t nb, int32_t* bcur, int4* stage, int32_t lo, int32_t hi,
-    const int4* __restrict__ sinfo = nullptr) {
+    bool slot_here = false, int32_t n = 0, const int4* __restrict__ sinfo = nullptr,
+    const unsigned long long* __restrict__ lmask = nullptr, const int32_t* __restrict__ off = nullptr) {
     __shared__ int32_t cnt[kMaxBuckets];
     __shared__ int32_t base[kMaxBuckets];
     for (int64_t t0 = (int64_t)blockIdx.x * kBucketTile; t0 < m; t0 += (int64_t)gridDim.x * kBucketTile) {
@@ -873,10 +873,14 @@ __global__ void __launch_bounds__(kBucketThreads) k_rev_bucket(
 #pragma unroll
         for (int k = 0; k < kBucketItems; ++k) {
             if (t[k] < 0) continue;
-            if (sinfo) {  // a[k] := the mark slot
-                const int4 q = sinfo[s[k]];
-                const unsigned long long w = ((unsigned long long)(uint32_t)q.y << 32) | (uint32_t)q.x;
-                a[k] = q.z + __popcll(w & ((1ull << (a[k] & 63)) - 1ull));
+            if (slot_here) {  // a[k] := the mark slot (bcrp.py:219)
+                if (sinfo) {
+                    const int4 q = sinfo[s[k]];
+                    const unsigned long long w = ((unsigned long long)(uint32_t)q.y << 32) | (uint32_t)q.x;
+                    a[k] = q.z + __popcll(w & ((1ull << (a[k] & 63)) - 1ull));
+                } else {
+                    a[k] = off[s[k]] + label_rank(lmask, n, s[k], a[k]);
+                }
             }
             r[k] = atomicAdd(&cnt[t[k] >> shift], 1);
         }
