@@ -56,7 +56,10 @@ __device__ __forceinline__ int32_t find_owner(const SparseParams& p, int32_t nbi
 // Owner list entry (and leader slot range) of chunk ci.  Up to 128 big
 // blocks the warp loads every entry at once and picks the owner by ballot,
 // one round trip instead of a base search followed by the entry load.
-constexpr int kEntryProbe = 4;  // entries per lane
+#ifndef BISIM_ENTRY_PROBE
+#define BISIM_ENTRY_PROBE 4
+#endif
+constexpr int kEntryProbe = BISIM_ENTRY_PROBE;  // entries per lane
 template <int K>
 __device__ __forceinline__ int32_t find_entry(const SparseParams& p, int32_t nbig, int32_t ci, int4& e, int2& li) {
     const int lane = threadIdx.x & 31;

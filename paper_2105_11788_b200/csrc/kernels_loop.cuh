@@ -21,6 +21,9 @@
 constexpr int32_t kSoloMaxC = 32;
 constexpr int32_t kSoloMaxItems = 256;
 constexpr int32_t kSoloSkipSpan = 512;   // skip-step window of the solo team: one label per thread
+#ifndef BISIM_PARK_NS
+#define BISIM_PARK_NS 64
+#endif
 #ifndef BISIM_KA
 #define BISIM_KA 1
 #endif
@@ -110,7 +113,7 @@ __global__ void __launch_bounds__(kSparseThreads, kSparsePerSm) k_refine_sparse(
                 // acknowledge: this CTA has read everything the solo decision
                 // used, CTA 0 may now modify the partition
                 asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&ctl->parked) : "memory");
-                while (ld_acquire_u32(&ctl->wake) == wakes) __nanosleep(64);
+                while (ld_acquire_u32(&ctl->wake) == wakes) __nanosleep(BISIM_PARK_NS);
             }
             __syncthreads();
             ++wakes;

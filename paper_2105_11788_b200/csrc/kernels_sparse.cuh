@@ -526,7 +526,10 @@ __device__ __forceinline__ bool set_first(uint32_t* bm, int32_t x, bool active) 
 // C usually share few source blocks, and thousands of warps hammering the
 // same tblock words serialise in L2.  Only the first inserter of b in a CTA
 // goes on to the grid-wide test-and-set.
-constexpr int kSeen = 1024;  // a multiple of the CTA size
+#ifndef BISIM_SEEN
+#define BISIM_SEEN 1024
+#endif
+constexpr int kSeen = BISIM_SEEN;  // a multiple of the CTA size
 
 // 0: b already seen by this CTA this round; 1: first insertion; 2: table
 // crowded (the global test-and-set decides).
