@@ -372,8 +372,11 @@ __global__ void __launch_bounds__(kSparseThreads, kSparsePerSm) k_refine_sparse(
 #pragma unroll
                     for (int u = 0; u < kA; ++u) {
                         if (k0 + 32 * u >= total) break;  // warp-uniform
-                        const unsigned same = __match_any_sync(kFull, act[u] ? b[u] : -1 - lane);
-                        const bool rep = act[u] && lane == __ffs(same) - 1;
+                        // a plain shared load first: a block this CTA already
+                        // met (the common case) skips the table's atomic; lanes
+                        // of one warp that miss on the same block race in
+                        // cta_first, which lets exactly one of them through
+                        const bool rep = act[u] && ld_vol(&s_seen[seen_slot(b[u])]) != b[u];
                         bool reg = false;
                         BlockInfo bi{};
                         if (rep) {

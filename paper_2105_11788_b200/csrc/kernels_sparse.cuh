@@ -533,8 +533,11 @@ constexpr int kSeen = BISIM_SEEN;  // a multiple of the CTA size
 
 // 0: b already seen by this CTA this round; 1: first insertion; 2: table
 // crowded (the global test-and-set decides).
+__device__ __forceinline__ uint32_t seen_slot(int32_t b) {
+    return ((uint32_t)b * 2654435761u) >> 22;  // 10-bit hash
+}
 __device__ __forceinline__ int cta_first(int32_t* seen, int32_t b) {
-    uint32_t h = ((uint32_t)b * 2654435761u) >> 22;  // 10-bit hash
+    uint32_t h = seen_slot(b);
 #pragma unroll 1
     for (int probe = 0; probe < 16; ++probe) {
         const int32_t old = atomicCAS(&seen[h], -1, b);

@@ -1,0 +1,146 @@
+// Phase-A cost breakdown on a c5-shaped heavy round (developer experiment):
+// walk the in-edges of an 89K-member splitter (in-degree 10, random sources
+// in n = 10M states, ~300 distinct source blocks) the way k_refine_sparse's
+// phase A does, with parts switched off, and time each variant.
+//   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o tools/phaseA_bench tools/phaseA_bench.cu
+#include <cstdint>
+#include <cstdio>
+#include <vector>
+#include <random>
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kSeen = 1024;
+
+__device__ __forceinline__ void red_or(uint32_t* a, uint32_t v) {
+    asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ int cta_first(int32_t* seen, int32_t b) {
+    uint32_t h = ((uint32_t)b * 2654435761u) >> 22;
+    for (int probe = 0; probe < 16; ++probe) {
+        const int32_t old = atomicCAS(&seen[h], -1, b);
+        if (old == -1) return 1;
+        if (old == b) return 0;
+        h = (h + 1) & (kSeen - 1);
+    }
+    return 2;
+}
+
+// flags: 1 mark red.or, 2 block gather, 4 match + cta hash, 8 byte-map mark store instead of bit red.or
+__global__ void __launch_bounds__(512, 1) walk(const int4* members, int32_t cz, const int2* rev, const int32_t* block,
+                                               uint32_t* mark, uint8_t* markb, int flags, unsigned long long* sink) {
+    __shared__ int32_t s_seen[kSeen];
+    for (int k = threadIdx.x; k < kSeen; k += blockDim.x) s_seen[k] = -1;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int32_t tw = (int32_t)((threadIdx.x >> 5) * gridDim.x + blockIdx.x);
+    const int32_t tnw = (int32_t)((gridDim.x * blockDim.x) >> 5);
+    int32_t g = max(1, (cz + tnw - 1) / tnw);
+    if (g > 32) {
+        const int32_t iters = (cz + tnw * 32 - 1) / (tnw * 32);
+        g = (cz + iters * tnw - 1) / (iters * tnw);
+    }
+    unsigned long long acc = 0;
+    for (int64_t i0 = (int64_t)tw * g; i0 < cz; i0 += (int64_t)tnw * g) {
+        const int64_t i = i0 + lane;
+        int32_t e0 = 0, d = 0;
+        if (lane < g && i < cz) {
+            const int4 r = members[i];
+            e0 = r.z;
+            d = r.w - r.z;
+        }
+        int32_t incl = d;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int32_t total = __shfl_sync(kFull, incl, 31);
+        const int32_t excl = incl - d;
+        for (int32_t k0 = 0; k0 < total; k0 += 32) {
+            const int32_t k = k0 + lane;
+            int32_t j = 0;
+#pragma unroll
+            for (int step = 16; step; step >>= 1) {
+                const int32_t ex = __shfl_sync(kFull, excl, j + step);
+                if (ex <= k) j += step;
+            }
+            const int32_t ej = __shfl_sync(kFull, e0, j);
+            const int32_t xj = __shfl_sync(kFull, excl, j);
+            const bool act = k < total;
+            const int2 rv = act ? __ldcs(&rev[ej + (k - xj)]) : make_int2(0, 0);
+            if (act && (flags & 1)) red_or(&mark[rv.x >> 5], 1u << (rv.x & 31));
+            if (act && (flags & 8)) markb[rv.x] = 1;
+            const int32_t b = (act && (flags & 2)) ? block[rv.y] : rv.y;
+            if (flags & 16) {  // plain shared load first, no match: only misses take the atomic path
+                if (act) {
+                    const uint32_t h = ((uint32_t)b * 2654435761u) >> 22;
+                    if (s_seen[h] != b) acc += (unsigned long long)cta_first(s_seen, b);
+                }
+            } else if (flags & 32) {  // match first, then plain load, then atomic
+                const unsigned same = __match_any_sync(kFull, act ? b : -1 - lane);
+                if (act && lane == __ffs(same) - 1) {
+                    const uint32_t h = ((uint32_t)b * 2654435761u) >> 22;
+                    if (s_seen[h] != b) acc += (unsigned long long)cta_first(s_seen, b);
+                }
+            } else if (flags & 4) {
+                const unsigned same = __match_any_sync(kFull, act ? b : -1 - lane);
+                if (act && lane == __ffs(same) - 1) acc += (unsigned long long)cta_first(s_seen, b);
+            } else {
+                acc += (unsigned long long)b;
+            }
+        }
+    }
+    if (acc == 0x123456789ull) sink[0] = acc;
+}
+
+int main() {
+    const int32_t n = 10000000, cz = 89000, deg = 10, nblocks = 300;
+    std::mt19937_64 rng(1);
+    std::vector<int4> mem(cz);
+    for (int32_t i = 0; i < cz; ++i) mem[i] = make_int4(i, 0, i * deg, (i + 1) * deg);
+    std::vector<int2> rev((size_t)cz * deg);
+    for (auto& r : rev) r = make_int2((int32_t)(rng() % (uint64_t)(5 * (uint64_t)n)), (int32_t)(rng() % n));
+    std::vector<int32_t> blk(n);
+    std::vector<int32_t> labels(nblocks);
+    for (auto& l : labels) l = (int32_t)(rng() % n);
+    for (auto& b : blk) b = labels[rng() % nblocks];
+    int4* d_mem;
+    int2* d_rev;
+    int32_t* d_blk;
+    uint32_t* d_mark;
+    uint8_t* d_markb;
+    unsigned long long* d_sink;
+    cudaMalloc(&d_mem, cz * 16);
+    cudaMalloc(&d_rev, rev.size() * 8);
+    cudaMalloc(&d_blk, (size_t)n * 4);
+    cudaMalloc(&d_mark, (size_t)5 * n / 8 + 64);
+    cudaMalloc(&d_markb, (size_t)5 * n + 64);
+    cudaMalloc(&d_sink, 8);
+    cudaMemcpy(d_mem, mem.data(), cz * 16, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_rev, rev.data(), rev.size() * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_blk, blk.data(), (size_t)n * 4, cudaMemcpyHostToDevice);
+    cudaMemset(d_mark, 0, (size_t)5 * n / 8 + 64);
+    cudaMemset(d_markb, 0, (size_t)5 * n + 64);
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const char* names[] = {"full (mark + gather + match/hash)", "no mark", "no match/hash",
+                           "rev loads only", "mark + gather, plain-load hash, no match",
+                           "mark + gather, match + plain-load hash"};
+    const int fl[] = {7, 6, 3, 0, 1 | 2 | 16, 1 | 2 | 32};
+    for (int v = 0; v < 6; ++v) {
+        for (int w = 0; w < 3; ++w) walk<<<sms, 512>>>(d_mem, cz, d_rev, d_blk, d_mark, d_markb, fl[v], d_sink);
+        const int R = 50;
+        cudaEventRecord(e0);
+        for (int r = 0; r < R; ++r) walk<<<sms, 512>>>(d_mem, cz, d_rev, d_blk, d_mark, d_markb, fl[v], d_sink);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        printf("%-40s %7.2f us per walk (%s)\n", names[v], ms * 1e3 / R, cudaGetErrorString(cudaGetLastError()));
+    }
+    return 0;
+}
