@@ -27,6 +27,7 @@ __device__ __forceinline__ int cta_first(int32_t* seen, int32_t b) {
 }
 
 // flags: 1 mark red.or, 2 block gather, 4 match + cta hash, 8 byte-map mark store instead of bit red.or
+template <int KA>
 __global__ void __launch_bounds__(512, 1) walk(const int4* members, int32_t cz, const int2* rev, const int32_t* block,
                                                uint32_t* mark, uint8_t* markb, int flags, unsigned long long* sink) {
     __shared__ int32_t s_seen[kSeen];
@@ -57,37 +58,43 @@ __global__ void __launch_bounds__(512, 1) walk(const int4* members, int32_t cz, 
         }
         const int32_t total = __shfl_sync(kFull, incl, 31);
         const int32_t excl = incl - d;
-        for (int32_t k0 = 0; k0 < total; k0 += 32) {
-            const int32_t k = k0 + lane;
-            int32_t j = 0;
+        for (int32_t k0 = 0; k0 < total; k0 += 32 * KA) {
+            int2 rv[KA];
+            bool act[KA];
 #pragma unroll
-            for (int step = 16; step; step >>= 1) {
-                const int32_t ex = __shfl_sync(kFull, excl, j + step);
-                if (ex <= k) j += step;
+            for (int u = 0; u < KA; ++u) {
+                const int32_t k = k0 + 32 * u + lane;
+                int32_t j = 0;
+#pragma unroll
+                for (int step = 16; step; step >>= 1) {
+                    const int32_t ex = __shfl_sync(kFull, excl, j + step);
+                    if (ex <= k) j += step;
+                }
+                const int32_t ej = __shfl_sync(kFull, e0, j);
+                const int32_t xj = __shfl_sync(kFull, excl, j);
+                act[u] = k < total;
+                rv[u] = act[u] ? __ldcs(&rev[ej + (k - xj)]) : make_int2(0, 0);
             }
-            const int32_t ej = __shfl_sync(kFull, e0, j);
-            const int32_t xj = __shfl_sync(kFull, excl, j);
-            const bool act = k < total;
-            const int2 rv = act ? __ldcs(&rev[ej + (k - xj)]) : make_int2(0, 0);
-            if (act && (flags & 1)) red_or(&mark[rv.x >> 5], 1u << (rv.x & 31));
-            if (act && (flags & 8)) markb[rv.x] = 1;
-            const int32_t b = (act && (flags & 2)) ? block[rv.y] : rv.y;
-            if (flags & 16) {  // plain shared load first, no match: only misses take the atomic path
-                if (act) {
-                    const uint32_t h = ((uint32_t)b * 2654435761u) >> 22;
-                    if (s_seen[h] != b) acc += (unsigned long long)cta_first(s_seen, b);
+            int32_t bb[KA];
+#pragma unroll
+            for (int u = 0; u < KA; ++u) {
+                if (act[u] && (flags & 1)) red_or(&mark[rv[u].x >> 5], 1u << (rv[u].x & 31));
+                bb[u] = (act[u] && (flags & 2)) ? block[rv[u].y] : rv[u].y;
+            }
+#pragma unroll
+            for (int u = 0; u < KA; ++u) {
+                const int32_t b = bb[u];
+                if (flags & 16) {
+                    if (act[u]) {
+                        const uint32_t h = ((uint32_t)b * 2654435761u) >> 22;
+                        if (s_seen[h] != b) acc += (unsigned long long)cta_first(s_seen, b);
+                    }
+                } else if (flags & 4) {
+                    const unsigned same = __match_any_sync(kFull, act[u] ? b : -1 - lane);
+                    if (act[u] && lane == __ffs(same) - 1) acc += (unsigned long long)cta_first(s_seen, b);
+                } else {
+                    acc += (unsigned long long)b;
                 }
-            } else if (flags & 32) {  // match first, then plain load, then atomic
-                const unsigned same = __match_any_sync(kFull, act ? b : -1 - lane);
-                if (act && lane == __ffs(same) - 1) {
-                    const uint32_t h = ((uint32_t)b * 2654435761u) >> 22;
-                    if (s_seen[h] != b) acc += (unsigned long long)cta_first(s_seen, b);
-                }
-            } else if (flags & 4) {
-                const unsigned same = __match_any_sync(kFull, act ? b : -1 - lane);
-                if (act && lane == __ffs(same) - 1) acc += (unsigned long long)cta_first(s_seen, b);
-            } else {
-                acc += (unsigned long long)b;
             }
         }
     }
@@ -127,15 +134,20 @@ int main() {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    const char* names[] = {"full (mark + gather + match/hash)", "no mark", "no match/hash",
-                           "rev loads only", "mark + gather, plain-load hash, no match",
-                           "mark + gather, match + plain-load hash"};
-    const int fl[] = {7, 6, 3, 0, 1 | 2 | 16, 1 | 2 | 32};
+    const char* names[] = {"KA1 match/hash (r01)", "KA1 plain-load hash (r02)", "KA2 plain-load hash",
+                           "KA4 plain-load hash", "KA1 no hash", "KA2 no hash"};
+    const int fl[] = {7, 1 | 2 | 16, 1 | 2 | 16, 1 | 2 | 16, 3, 3};
+    const int ka[] = {1, 1, 2, 4, 1, 2};
     for (int v = 0; v < 6; ++v) {
-        for (int w = 0; w < 3; ++w) walk<<<sms, 512>>>(d_mem, cz, d_rev, d_blk, d_mark, d_markb, fl[v], d_sink);
+        auto launch = [&]() {
+            if (ka[v] == 1) walk<1><<<sms, 512>>>(d_mem, cz, d_rev, d_blk, d_mark, d_markb, fl[v], d_sink);
+            else if (ka[v] == 2) walk<2><<<sms, 512>>>(d_mem, cz, d_rev, d_blk, d_mark, d_markb, fl[v], d_sink);
+            else walk<4><<<sms, 512>>>(d_mem, cz, d_rev, d_blk, d_mark, d_markb, fl[v], d_sink);
+        };
+        for (int w = 0; w < 3; ++w) launch();
         const int R = 50;
         cudaEventRecord(e0);
-        for (int r = 0; r < R; ++r) walk<<<sms, 512>>>(d_mem, cz, d_rev, d_blk, d_mark, d_markb, fl[v], d_sink);
+        for (int r = 0; r < R; ++r) launch();
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms;
