@@ -39,6 +39,116 @@ constexpr int32_t kSkipGain = BISIM_SKIP_GAIN;  // rounds a skip step must retir
 // in-edges per lane per phase-A step: 1 since the fat barriers (process-level
 // A/B vs 2: c1 -3.2 %, c2 -2.0 %, c4l -1.5 %, c3 -1.1 %, c5 / c4u -0.1 %; 3: slower)
 constexpr int kA = BISIM_KA;
+#ifndef BISIM_KA_BATCH
+#define BISIM_KA_BATCH 4
+#endif
+constexpr int kABatch = BISIM_KA_BATCH;  // ... for splitters of >= batch_min_c members
+
+// Phase A walk over C's members [cs, cs + cz): g members per warp and
+// iteration, their in-edges spread over the lanes (warp scan of in-degrees),
+// KA in-edges per lane per step issued together.  Marks every in-edge's slot
+// and registers each source block once (see the kernel below).
+template <int KA, bool IDENT, bool SH>
+__device__ __forceinline__ void walk_members(const SparseParams& p, int cur, int32_t cs, int32_t cz, int32_t tw,
+                                             int32_t tnw, int32_t g, bool solo, bool batch, int32_t* s_seen,
+                                             unsigned long long& my_edges) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t i0 = (int64_t)tw * g; i0 < cz; i0 += (int64_t)tnw * g) {
+        const int64_t i = i0 + lane;
+        int32_t e0 = 0, d = 0;
+        if (lane < g && i < cz) {
+            const MemberRec r = p.members[cs + i];
+            e0 = r.z;
+            d = r.w - r.z;
+        }
+        int32_t incl = d;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int32_t total = __shfl_sync(kFull, incl, 31);
+        const int32_t excl = incl - d;
+        my_edges += (unsigned long long)d;
+        // KA in-edges per lane per step: their loads are issued
+        // together (reverse edges, then source blocks), so a warp
+        // walking a big splitter keeps KA dependent chains in flight
+        for (int32_t k0 = 0; k0 < total; k0 += 32 * KA) {
+            int32_t s[KA], b[KA];
+            bool act[KA];
+#pragma unroll
+            for (int u = 0; u < KA; ++u) {
+                const int32_t k = k0 + 32 * u + lane;
+                if (k0 + 32 * u >= total) {  // warp-uniform: nothing left
+                    act[u] = false;
+                    s[u] = -1;
+                    continue;
+                }
+                // owner lane j: the last lane with excl_j <= k
+                int32_t j = 0;
+#pragma unroll
+                for (int step = 16; step; step >>= 1) {
+                    const int32_t ex = __shfl_sync(kFull, excl, j + step);
+                    if (ex <= k) j += step;
+                }
+                const int32_t ej = __shfl_sync(kFull, e0, j);
+                const int32_t xj = __shfl_sync(kFull, excl, j);
+                act[u] = k < total;
+                s[u] = act[u] ? ej + (k - xj) : -1;  // the in-edge index, for now
+            }
+            int2 rv[KA];
+#pragma unroll
+            for (int u = 0; u < KA; ++u) {
+                // reverse edges stream through (evict-first), so they do not push
+                // the randomly accessed per-state arrays out of L2
+                if (IDENT) rv[u] = make_int2(0, act[u] ? __ldcs(&p.rev_src[s[u]]) : 0);
+                else rv[u] = act[u] ? __ldcs(&p.rev[s[u]]) : make_int2(0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < KA; ++u) {
+                s[u] = rv[u].y;
+                const int32_t slot = IDENT ? s[u] : rv[u].x;
+                if (act[u]) {
+                    if (SH) shard_mark(p, cur, slot);
+                    else red_or(&p.mark[slot >> 5], 1u << (slot & 31));
+                }
+                b[u] = act[u] ? p.block[s[u]] : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < KA; ++u) {
+                if (k0 + 32 * u >= total) break;  // warp-uniform
+                // a plain shared load first: a block this CTA already
+                // met (the common case) skips the table's atomic; lanes
+                // of one warp that miss on the same block race in
+                // cta_first, which lets exactly one of them through
+                const bool rep = act[u] && ld_vol(&s_seen[seen_slot(b[u])]) != b[u];
+                bool reg = false;
+                BlockInfo bi{};
+                if (rep) {
+                    const int f = cta_first(s_seen, b[u]);
+                    if (f == 1 && solo) {
+                        reg = true;  // the solo team is this CTA: its table is exact
+                        bi = block_info(p, b[u]);
+                    } else if (f == 2 || (f == 1 && !batch)) {
+                        // the block's info loads overlap the test-and-set
+#ifndef BISIM_NO_PRE
+                        bi = block_info(p, b[u]);
+#endif
+                        const uint32_t bit = 1u << (b[u] & 31);
+                        reg = !(atomicOr(&p.tblock[b[u] >> 5], bit) & bit);
+                    }
+                }
+                if (__any_sync(kFull, reg)) {
+#ifdef BISIM_NO_PRE
+                    if (reg) bi = block_info(p, b[u]);
+#endif
+                    register_blocks_warp(p, cur, reg, b[u], bi, solo);
+                    if (SH && reg) shard_publish(p, cur, b[u]);
+                }
+            }
+        }
+    }
+}
 
 template <bool IDENT, bool SH>
 __global__ void __launch_bounds__(kSparseThreads, kSparsePerSm) k_refine_sparse(SparseParams pk) {
@@ -308,101 +418,10 @@ __global__ void __launch_bounds__(kSparseThreads, kSparsePerSm) k_refine_sparse(
                 const int32_t iters = (cz + tnw * 32 - 1) / (tnw * 32);
                 g = (cz + iters * tnw - 1) / (iters * tnw);
             }
-            for (int64_t i0 = (int64_t)tw * g; i0 < cz; i0 += (int64_t)tnw * g) {
-                const int64_t i = i0 + lane;
-                int32_t e0 = 0, d = 0;
-                if (lane < g && i < cz) {
-                    const MemberRec r = p.members[cs + i];
-                    e0 = r.z;
-                    d = r.w - r.z;
-                }
-                int32_t incl = d;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int32_t y = __shfl_up_sync(kFull, incl, o);
-                    if (lane >= o) incl += y;
-                }
-                const int32_t total = __shfl_sync(kFull, incl, 31);
-                const int32_t excl = incl - d;
-                my_edges += (unsigned long long)d;
-                // kA in-edges per lane per step: their loads are issued
-                // together (reverse edges, then source blocks), so a warp
-                // walking a big splitter keeps kA dependent chains in flight
-                for (int32_t k0 = 0; k0 < total; k0 += 32 * kA) {
-                    int32_t s[kA], b[kA];
-                    bool act[kA];
-#pragma unroll
-                    for (int u = 0; u < kA; ++u) {
-                        const int32_t k = k0 + 32 * u + lane;
-                        if (k0 + 32 * u >= total) {  // warp-uniform: nothing left
-                            act[u] = false;
-                            s[u] = -1;
-                            continue;
-                        }
-                        // owner lane j: the last lane with excl_j <= k
-                        int32_t j = 0;
-#pragma unroll
-                        for (int step = 16; step; step >>= 1) {
-                            const int32_t ex = __shfl_sync(kFull, excl, j + step);
-                            if (ex <= k) j += step;
-                        }
-                        const int32_t ej = __shfl_sync(kFull, e0, j);
-                        const int32_t xj = __shfl_sync(kFull, excl, j);
-                        act[u] = k < total;
-                        s[u] = act[u] ? ej + (k - xj) : -1;  // the in-edge index, for now
-                    }
-                    int2 rv[kA];
-#pragma unroll
-                    for (int u = 0; u < kA; ++u) {
-                        // reverse edges stream through (evict-first), so they do not push
-                        // the randomly accessed per-state arrays out of L2
-                        if (IDENT) rv[u] = make_int2(0, act[u] ? __ldcs(&p.rev_src[s[u]]) : 0);
-                        else rv[u] = act[u] ? __ldcs(&p.rev[s[u]]) : make_int2(0, 0);
-                    }
-#pragma unroll
-                    for (int u = 0; u < kA; ++u) {
-                        s[u] = rv[u].y;
-                        const int32_t slot = IDENT ? s[u] : rv[u].x;
-                        if (act[u]) {
-                            if (SH) shard_mark(p, cur, slot);
-                            else red_or(&p.mark[slot >> 5], 1u << (slot & 31));
-                        }
-                        b[u] = act[u] ? p.block[s[u]] : 0;
-                    }
-#pragma unroll
-                    for (int u = 0; u < kA; ++u) {
-                        if (k0 + 32 * u >= total) break;  // warp-uniform
-                        // a plain shared load first: a block this CTA already
-                        // met (the common case) skips the table's atomic; lanes
-                        // of one warp that miss on the same block race in
-                        // cta_first, which lets exactly one of them through
-                        const bool rep = act[u] && ld_vol(&s_seen[seen_slot(b[u])]) != b[u];
-                        bool reg = false;
-                        BlockInfo bi{};
-                        if (rep) {
-                            const int f = cta_first(s_seen, b[u]);
-                            if (f == 1 && solo) {
-                                reg = true;  // the solo team is this CTA: its table is exact
-                                bi = block_info(p, b[u]);
-                            } else if (f == 2 || (f == 1 && !batch)) {
-                                // the block's info loads overlap the test-and-set
-#ifndef BISIM_NO_PRE
-                                bi = block_info(p, b[u]);
-#endif
-                                const uint32_t bit = 1u << (b[u] & 31);
-                                reg = !(atomicOr(&p.tblock[b[u] >> 5], bit) & bit);
-                            }
-                        }
-                        if (__any_sync(kFull, reg)) {
-#ifdef BISIM_NO_PRE
-                            if (reg) bi = block_info(p, b[u]);
-#endif
-                            register_blocks_warp(p, cur, reg, b[u], bi, solo);
-                            if (SH && reg) shard_publish(p, cur, b[u]);
-                        }
-                    }
-                }
-            }
+            // big splitters keep several in-edges per lane in flight; the
+            // latency-bound small ones are fastest with one
+            if (batch) walk_members<kABatch, IDENT, SH>(p, cur, cs, cz, tw, tnw, g, solo, batch, s_seen, my_edges);
+            else walk_members<kA, IDENT, SH>(p, cur, cs, cz, tw, tnw, g, solo, batch, s_seen, my_edges);
             if (batch) {
                 // a huge splitter: the CTA's table holds every source block
                 // its warps met; one wave of global test-and-sets registers
