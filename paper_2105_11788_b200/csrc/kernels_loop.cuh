@@ -538,11 +538,11 @@ __global__ void __launch_bounds__(kSparseThreads, kSparsePerSm) k_refine_sparse(
                 else cnt = big_tag<IDENT, kWide>(p, nbig, it - nsm);
                 if (lane == 0) my_members += (unsigned long long)cnt;
             }
-            trace_at(p, round, 13);  // CTA 0's warp 0 done with pass 1
+            trace_at(p, round, 8);  // CTA 0's warp 0 done with pass 1
             team_barrier(solo, p.bar, gen, [] {});
-            trace_at(p, round, 14);
+            trace_at(p, round, 9);
             for (int32_t it = tw; it < nch; it += tnw) big_split<IDENT, kWide>(p, cur, round, C, nbig, it);
-            trace_at(p, round, 15);
+            trace_at(p, round, 10);
         } else {
             // one pass: every work item has its own warp; all warps of the
             // CTA take part (the big-chunk path synchronises the CTA)

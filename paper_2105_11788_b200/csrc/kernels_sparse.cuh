@@ -230,8 +230,9 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // Developer trace (BISIM_TRACE): kTraceWords words per round, written by
 // thread 0 of CTA 0: [0..3] round start / end of phase A / after the A
 // barrier / after the B barrier, [4..7] counters, [8..12] phase-B steps of
-// the one-pass path (tagged, CTA-synced, arrived, cursors synced, done),
-// [13..15] of the two-pass path (pass 1 done, mid barrier passed, pass 2 done).
+// the one-pass path (tagged, CTA-synced, arrived, cursors synced, done) or
+// [8..10] of the two-pass path (pass 1 done, mid barrier passed, pass 2
+// done), [13] the round's phase-B mode.
 constexpr int kTraceWords = 16;
 __device__ __forceinline__ void trace_at(const SparseParams& p, int64_t round, int k) {
     if (p.trace && blockIdx.x == 0 && threadIdx.x == 0 && round < p.trace_rounds)
