@@ -838,7 +838,7 @@ int run_with(Ctx& c, Job& j) {
         sp.onepass_major = dev_env("BISIM_ONEPASS_MINOR") != nullptr ? 0
                            : dev_env("BISIM_MAJOR") ? atoi(dev_env("BISIM_MAJOR")) : kSparseThreads / 32;
         sp.wide_major = dev_env("BISIM_WIDE_MAJOR") ? atoi(dev_env("BISIM_WIDE_MAJOR")) : 0;
-        sp.prefetch_next = dev_env("BISIM_PREFETCH") ? atoi(dev_env("BISIM_PREFETCH")) : 1;
+        sp.prefetch_next = dev_env("BISIM_PREFETCH") ? atoi(dev_env("BISIM_PREFETCH")) : 2;
         sp.solo_max_c = dev_env("BISIM_SOLO_C") ? atoi(dev_env("BISIM_SOLO_C")) : kSoloMaxC;
         sp.solo_max_items = dev_env("BISIM_SOLO_ITEMS") ? atoi(dev_env("BISIM_SOLO_ITEMS")) : kSoloMaxItems;
         // developer tracing: BISIM_TRACE=<rounds> BISIM_TRACE_FILE=<path>
@@ -885,6 +885,8 @@ int run_with(Ctx& c, Job& j) {
     } else {
         kfn = j.bcrp ? (const void*)k_refine_sparse<false, false> : (const void*)k_refine_sparse<true, false>;
         kgrid = j.bcrp ? c.grid_sparse_bcrp : c.grid_sparse_rcpp;
+        // developer: BISIM_SPARSE_GRID=<CTAs> (at most the resident grid)
+        if (const char* g = dev_env("BISIM_SPARSE_GRID")) kgrid = std::max(1, std::min(kgrid, atoi(g)));
         kthreads = kSparseThreads;
         kargs[0] = &sp;
     }

@@ -557,6 +557,26 @@ __global__ void __launch_bounds__(kSparseThreads, kSparsePerSm) k_refine_sparse(
             int32_t it = twb - nch;
             if (it < 0) it += tnw;
             for (; it < nsm; it += tnw) cnt += process_small<IDENT>(p, cur, round, C, p.small_list[it]);
+            // warps without an item pull the in-edges of C's successor (the
+            // usual next splitter, its range published in phase A) towards
+            // L2, a warp per 32 of its members: phase A of the next round
+            // then finds them there instead of in HBM (a hint only: a
+            // different next splitter just leaves the lines unused).  Only in
+            // rounds without small touched blocks: their splits raise the
+            // labels that usually come next instead (c2: no gain)
+            if (p.prefetch_next >= 2 && !solo && nsm == 0 && twb >= nch) {
+                const unsigned* rec = ctl->brec[cur];
+                const int32_t sx = (int32_t)(ld_vol(&rec[2]) & ~kRecFlag), sz = (int32_t)(ld_vol(&rec[3]) & ~kRecFlag);
+                const int32_t i = (twb - nch) * 32 + lane;
+                if (i < sz) {
+                    const MemberRec r = p.members[sx + i];
+                    const char* a = IDENT ? (const char*)(p.rev_src + r.z) : (const char*)(p.rev + r.z);
+                    const char* e = IDENT ? (const char*)(p.rev_src + r.w) : (const char*)(p.rev + r.w);
+                    a = (const char*)((uintptr_t)a & ~(uintptr_t)127);
+                    for (int k = 0; k < 4 && a < e; ++k, a += 128)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+                }
+            }
             const int32_t ci = twb < nch ? twb : -1;
             if (mode_b == 0) cnt += big_onepass_cta<IDENT, 1>(p, cur, round, C, nbig, ci, s_slot);
             else cnt += big_onepass_cta<IDENT, kWide>(p, cur, round, C, nbig, ci, s_slot);

@@ -206,7 +206,7 @@ struct SparseParams {
     int32_t batch_min_c;        // splitter size from which phase A registers blocks in one wave
     int32_t onepass_major;      // one-pass phase B: CTA-major item placement up to this many chunks per big block
     int32_t wide_major;         // ... and the wide layout when its chunks per big block are at most this
-    int32_t prefetch_next;      // phase A: prefetch the likely next splitter's member records
+    int32_t prefetch_next;      // prefetch the likely next splitter's member records (1: in phase A) and in-edges (2: + phase B)
     // ---- transition-sharded mode (kernels_shard.cuh); nshard == 1 otherwise
     int32_t nshard;                       // replicas taking part in every round
     int32_t shard;                        // my index

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <vector>
 #include <random>
+#include <cstdlib>
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kSeen = 1024;
@@ -104,9 +105,20 @@ __global__ void __launch_bounds__(512, 1) walk(const int4* members, int32_t cz, 
 int main() {
     const int32_t n = 10000000, cz = 89000, deg = 10, nblocks = 300;
     std::mt19937_64 rng(1);
-    std::vector<int4> mem(cz);
-    for (int32_t i = 0; i < cz; ++i) mem[i] = make_int4(i, 0, i * deg, (i + 1) * deg);
-    std::vector<int2> rev((size_t)cz * deg);
+    // spread=1: every member's in-edge range at a random place of a c5-sized
+    // (100M-entry, 800 MB) reverse CSR, as in the loop, instead of packed
+    // into 7 MB that stays in L2 across repetitions
+    const bool spread = getenv("SPREAD") != nullptr;
+    // (and a different splitter each repetition, so its in-edges are not
+    // the ones the previous repetition left in L2)
+    const size_t nrev = spread ? (size_t)100000000 : (size_t)cz * deg;
+    const int nset = spread ? 50 : 1;
+    std::vector<int4> mem((size_t)cz * nset);
+    for (size_t i = 0; i < mem.size(); ++i) {
+        const int32_t e0 = spread ? (int32_t)(rng() % (nrev / deg)) * deg : (int32_t)i * deg;
+        mem[i] = make_int4((int32_t)(i % cz), 0, e0, e0 + deg);
+    }
+    std::vector<int2> rev(nrev);
     for (auto& r : rev) r = make_int2((int32_t)(rng() % (uint64_t)(5 * (uint64_t)n)), (int32_t)(rng() % n));
     std::vector<int32_t> blk(n);
     std::vector<int32_t> labels(nblocks);
@@ -118,13 +130,13 @@ int main() {
     uint32_t* d_mark;
     uint8_t* d_markb;
     unsigned long long* d_sink;
-    cudaMalloc(&d_mem, cz * 16);
+    cudaMalloc(&d_mem, mem.size() * 16);
     cudaMalloc(&d_rev, rev.size() * 8);
     cudaMalloc(&d_blk, (size_t)n * 4);
     cudaMalloc(&d_mark, (size_t)5 * n / 8 + 64);
     cudaMalloc(&d_markb, (size_t)5 * n + 64);
     cudaMalloc(&d_sink, 8);
-    cudaMemcpy(d_mem, mem.data(), cz * 16, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_mem, mem.data(), mem.size() * 16, cudaMemcpyHostToDevice);
     cudaMemcpy(d_rev, rev.data(), rev.size() * 8, cudaMemcpyHostToDevice);
     cudaMemcpy(d_blk, blk.data(), (size_t)n * 4, cudaMemcpyHostToDevice);
     cudaMemset(d_mark, 0, (size_t)5 * n / 8 + 64);
@@ -139,10 +151,12 @@ int main() {
     const int fl[] = {7, 1 | 2 | 16, 1 | 2 | 16, 1 | 2 | 16, 3, 3};
     const int ka[] = {1, 1, 2, 4, 1, 2};
     for (int v = 0; v < 6; ++v) {
+        int rep = 0;
         auto launch = [&]() {
-            if (ka[v] == 1) walk<1><<<sms, 512>>>(d_mem, cz, d_rev, d_blk, d_mark, d_markb, fl[v], d_sink);
-            else if (ka[v] == 2) walk<2><<<sms, 512>>>(d_mem, cz, d_rev, d_blk, d_mark, d_markb, fl[v], d_sink);
-            else walk<4><<<sms, 512>>>(d_mem, cz, d_rev, d_blk, d_mark, d_markb, fl[v], d_sink);
+            const int4* m = d_mem + (size_t)(rep++ % nset) * cz;
+            if (ka[v] == 1) walk<1><<<sms, 512>>>(m, cz, d_rev, d_blk, d_mark, d_markb, fl[v], d_sink);
+            else if (ka[v] == 2) walk<2><<<sms, 512>>>(m, cz, d_rev, d_blk, d_mark, d_markb, fl[v], d_sink);
+            else walk<4><<<sms, 512>>>(m, cz, d_rev, d_blk, d_mark, d_markb, fl[v], d_sink);
         };
         for (int w = 0; w < 3; ++w) launch();
         const int R = 50;
