@@ -977,13 +977,14 @@ int run_with(Ctx& c, Job& j) {
         const char* path = dev_env("BISIM_TRACE_FILE");
         if (FILE* f = fopen(path ? path : "bisim_trace.csv", "w")) {
             fprintf(f, "round,phaseA_ns,barrierA_ns,phaseB_ns,csize,solo,n_small,big_chunks,n_big,"
-                       "b_tag_ns,b_sync1_ns,b_arrive_ns,b_sync2_ns,b_place_ns,mode_b\n");
+                       "b_tag_ns,b_sync1_ns,b_arrive_ns,b_sync2_ns,b_place_ns,mode_b,a_walk0_ns,a_walkcta_ns,a_wave_ns\n");
             for (int64_t r = 0; r < std::min<int64_t>(sp.trace_rounds, R); ++r) {
                 const unsigned long long* q = &t[r * kTraceWords];
                 auto d = [&](int a, int b) -> long long { return (q[a] && q[b]) ? (long long)(q[a] - q[b]) : -1; };
-                fprintf(f, "%lld,%llu,%llu,%llu,%llu,%llu,%llu,%llu,%llu,%lld,%lld,%lld,%lld,%lld,%llu\n", (long long)r,
-                        q[1] - q[0], q[2] - q[1], q[3] - q[2], q[4], q[5], q[6], q[7] & 0xffffffffull, q[7] >> 32,
-                        d(8, 2), d(9, 8), d(10, 9), d(11, 10), d(12, 11), q[13]);
+                fprintf(f, "%lld,%llu,%llu,%llu,%llu,%llu,%llu,%llu,%llu,%lld,%lld,%lld,%lld,%lld,%llu,%lld,%lld,%lld\n",
+                        (long long)r, q[1] - q[0], q[2] - q[1], q[3] - q[2], q[4], q[5], q[6],
+                        q[7] & 0xffffffffull, q[7] >> 32, d(8, 2), d(9, 8), d(10, 9), d(11, 10), d(12, 11),
+                        q[13], d(14, 0), d(15, 14), d(1, 15));
             }
             fclose(f);
         }

@@ -426,9 +426,17 @@ __global__ void __launch_bounds__(kSparseThreads, kSparsePerSm) k_refine_sparse(
                 // a huge splitter: the CTA's table holds every source block
                 // its warps met; one wave of global test-and-sets registers
                 // them, instead of a returning atomic inside the walk's steps
+                trace_at(p, round, 14);  // warp 0's walk done
                 __syncthreads();
-                for (int k0 = 0; k0 < kSeen; k0 += blockDim.x) {
-                    const int k = k0 + threadIdx.x;
+                trace_at(p, round, 15);  // the CTA's walk done
+                // the same source blocks sit in the same slots of every
+                // CTA's table: odd CTAs take the table's second half first, so
+                // half of the test-and-sets of a hot word find it set by a
+                // plain load instead of queueing on it
+                constexpr int kPer = kSeen / kSparseThreads;
+                static_assert(kSeen % kSparseThreads == 0, "table entries per thread");
+                for (int q = 0; q < kPer; ++q) {
+                    const int k = ((q + (int)(blockIdx.x & 1u) * (kPer / 2)) % kPer) * kSparseThreads + threadIdx.x;
                     const int32_t b = s_seen[k];
                     bool reg = false;
                     if (b >= 0) {

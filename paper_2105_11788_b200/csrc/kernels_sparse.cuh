@@ -232,7 +232,8 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // barrier / after the B barrier, [4..7] counters, [8..12] phase-B steps of
 // the one-pass path (tagged, CTA-synced, arrived, cursors synced, done) or
 // [8..10] of the two-pass path (pass 1 done, mid barrier passed, pass 2
-// done), [13] the round's phase-B mode.
+// done), [13] the round's phase-B mode, [14..15] batch phase A (warp 0's
+// walk done, the CTA's walk done).
 constexpr int kTraceWords = 16;
 __device__ __forceinline__ void trace_at(const SparseParams& p, int64_t round, int k) {
     if (p.trace && blockIdx.x == 0 && threadIdx.x == 0 && round < p.trace_rounds)
