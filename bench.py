@@ -115,6 +115,13 @@ class ClockSampler:
             self.t.start()
         except OSError:
             self.proc = None
+            return self
+        # nvidia-smi needs ~0.5-1 s to start: wait for its first sample, so
+        # a short timed region (the default 5 steps ~0.45 s) is still sampled
+        t0 = time.perf_counter()
+        while not self.lines and self.proc.poll() is None and time.perf_counter() - t0 < 10.0:
+            time.sleep(0.02)
+        self.lines.clear()  # keep only samples taken inside the timed region
         return self
 
     def _read(self):
