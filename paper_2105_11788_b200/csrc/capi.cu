@@ -839,6 +839,8 @@ int run_with(Ctx& c, Job& j) {
                            : dev_env("BISIM_MAJOR") ? atoi(dev_env("BISIM_MAJOR")) : kSparseThreads / 32;
         sp.wide_major = dev_env("BISIM_WIDE_MAJOR") ? atoi(dev_env("BISIM_WIDE_MAJOR")) : 0;
         sp.prefetch_next = dev_env("BISIM_PREFETCH") ? atoi(dev_env("BISIM_PREFETCH")) : 2;
+        // one-pass wide layout above 512 chunks of 32 per big block (A/B: 32 -> c5 +9 %, 128 -> neutral)
+        sp.wide_min = dev_env("BISIM_WIDE_MIN") ? atoi(dev_env("BISIM_WIDE_MIN")) : 512;
         sp.solo_max_c = dev_env("BISIM_SOLO_C") ? atoi(dev_env("BISIM_SOLO_C")) : kSoloMaxC;
         sp.solo_max_items = dev_env("BISIM_SOLO_ITEMS") ? atoi(dev_env("BISIM_SOLO_ITEMS")) : kSoloMaxItems;
         // developer tracing: BISIM_TRACE=<rounds> BISIM_TRACE_FILE=<path>

@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(kSparseThreads, kSparsePerSm) k_refine_sparse(
                 s_snap[0] = (int32_t)w1;
                 s_snap[1] = (long long)(((unsigned long long)w3 << 32) | w2);
                 const int32_t nb = (int32_t)w3, n1 = (int32_t)w2, tw_all = (int32_t)(blockDim.x >> 5) * gridDim.x;
-                const bool need4 = n1 > tw_all || n1 > 512 * nb || p.wide_major > 0 || p.force_mode_b > 0;
+                const bool need4 = n1 > tw_all || n1 > p.wide_min * nb || p.wide_major > 0 || p.force_mode_b > 0;
                 s_snap[2] = need4 ? (long long)ld_vol(&ctl->big_pack4[cur]) : 0ll;
             }
             if (cur) ++genA1;
@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(kSparseThreads, kSparsePerSm) k_refine_sparse(
         // a few very large blocks (> 16K members each on average): the wide
         // layout keeps a quarter of the warps busy with 4 loads in flight per
         // lane, which measured faster than every warp holding one chunk
-        if (mode_b == 0 && nch1 > 512 * nbig) mode_b = 1;
+        if (mode_b == 0 && nch1 > p.wide_min * nbig) mode_b = 1;
         // blocks of a few wide chunks each: the wide layout with CTA-major
         // placement keeps most blocks inside one CTA, whose chunks combine
         // in shared memory instead of a global arrival

@@ -207,6 +207,7 @@ struct SparseParams {
     int32_t onepass_major;      // one-pass phase B: CTA-major item placement up to this many chunks per big block
     int32_t wide_major;         // ... and the wide layout when its chunks per big block are at most this
     int32_t prefetch_next;      // prefetch the likely next splitter's member records (1: in phase A) and in-edges (2: + phase B)
+    int32_t wide_min;           // one-pass phase B takes the wide layout above this many 32-member chunks per big block
     // ---- transition-sharded mode (kernels_shard.cuh); nshard == 1 otherwise
     int32_t nshard;                       // replicas taking part in every round
     int32_t shard;                        // my index

@@ -8,6 +8,7 @@
 #include <vector>
 #include <random>
 #include <cstdlib>
+#include <algorithm>
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kSeen = 1024;
@@ -28,7 +29,13 @@ __device__ __forceinline__ int cta_first(int32_t* seen, int32_t b) {
 }
 
 // flags: 1 mark red.or, 2 block gather, 4 match + cta hash, 8 byte-map mark store instead of bit red.or
-template <int KA>
+__device__ unsigned long long g_t[2][148 * 16];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+template <int KA, bool PF = false>
 __global__ void __launch_bounds__(512, 1) walk(const int4* members, int32_t cz, const int2* rev, const int32_t* block,
                                                uint32_t* mark, uint8_t* markb, int flags, unsigned long long* sink) {
     __shared__ int32_t s_seen[kSeen];
@@ -36,6 +43,7 @@ __global__ void __launch_bounds__(512, 1) walk(const int4* members, int32_t cz, 
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int32_t tw = (int32_t)((threadIdx.x >> 5) * gridDim.x + blockIdx.x);
+    if (lane == 0) g_t[0][tw] = gtimer();
     const int32_t tnw = (int32_t)((gridDim.x * blockDim.x) >> 5);
     int32_t g = max(1, (cz + tnw - 1) / tnw);
     if (g > 32) {
@@ -43,10 +51,17 @@ __global__ void __launch_bounds__(512, 1) walk(const int4* members, int32_t cz, 
         g = (cz + iters * tnw - 1) / (iters * tnw);
     }
     unsigned long long acc = 0;
+    int4 nx = make_int4(0, 0, 0, 0);
+    if (PF && lane < g && (int64_t)tw * g + lane < cz) nx = members[(int64_t)tw * g + lane];
     for (int64_t i0 = (int64_t)tw * g; i0 < cz; i0 += (int64_t)tnw * g) {
         const int64_t i = i0 + lane;
         int32_t e0 = 0, d = 0;
-        if (lane < g && i < cz) {
+        if (PF) {
+            e0 = nx.z;
+            d = nx.w - nx.z;
+            const int64_t i2 = i + (int64_t)tnw * g;
+            nx = (lane < g && i2 < cz) ? members[i2] : make_int4(0, 0, 0, 0);
+        } else if (lane < g && i < cz) {
             const int4 r = members[i];
             e0 = r.z;
             d = r.w - r.z;
@@ -79,8 +94,13 @@ __global__ void __launch_bounds__(512, 1) walk(const int4* members, int32_t cz, 
             int32_t bb[KA];
 #pragma unroll
             for (int u = 0; u < KA; ++u) {
-                if (act[u] && (flags & 1)) red_or(&mark[rv[u].x >> 5], 1u << (rv[u].x & 31));
+                if (!(flags & 32) && act[u] && (flags & 1)) red_or(&mark[rv[u].x >> 5], 1u << (rv[u].x & 31));
                 bb[u] = (act[u] && (flags & 2)) ? block[rv[u].y] : rv[u].y;
+            }
+            if (flags & 32) {  // block gathers first, then the marks
+#pragma unroll
+                for (int u = 0; u < KA; ++u)
+                    if (act[u] && (flags & 1)) red_or(&mark[rv[u].x >> 5], 1u << (rv[u].x & 31));
             }
 #pragma unroll
             for (int u = 0; u < KA; ++u) {
@@ -100,6 +120,51 @@ __global__ void __launch_bounds__(512, 1) walk(const int4* members, int32_t cz, 
         }
     }
     if (acc == 0x123456789ull) sink[0] = acc;
+    if (lane == 0) g_t[1][tw] = gtimer();
+}
+
+// lane-per-member walk: every lane walks its own member's in-edges, E at a
+// time (loads issued together), instead of a warp scan spreading a group of
+// members' in-edges over the lanes
+template <int E>
+__global__ void __launch_bounds__(512, 1) walk_lane(const int4* members, int32_t cz, const int2* rev,
+                                                    const int32_t* block, uint32_t* mark, int flags,
+                                                    unsigned long long* sink) {
+    __shared__ int32_t s_seen[kSeen];
+    for (int k = threadIdx.x; k < kSeen; k += blockDim.x) s_seen[k] = -1;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int32_t tw = (int32_t)((threadIdx.x >> 5) * gridDim.x + blockIdx.x);
+    if (lane == 0) g_t[0][tw] = gtimer();
+    const int64_t gl = (int64_t)tw * 32 + lane, nl = (int64_t)gridDim.x * blockDim.x;
+    unsigned long long acc = 0;
+    for (int64_t i = gl; i < cz; i += nl) {
+        const int4 r = members[i];
+        for (int32_t e = r.z; e < r.w; e += E) {
+            int2 rv[E];
+            int32_t bb[E];
+#pragma unroll
+            for (int u = 0; u < E; ++u) rv[u] = e + u < r.w ? __ldcs(&rev[e + u]) : make_int2(0, -1);
+#pragma unroll
+            for (int u = 0; u < E; ++u) {
+                if (rv[u].y >= 0 && (flags & 1)) red_or(&mark[rv[u].x >> 5], 1u << (rv[u].x & 31));
+                bb[u] = (rv[u].y >= 0 && (flags & 2)) ? block[rv[u].y] : rv[u].y;
+            }
+#pragma unroll
+            for (int u = 0; u < E; ++u) {
+                const int32_t b = bb[u];
+                if (rv[u].y < 0) continue;
+                if (flags & 16) {
+                    const uint32_t h = ((uint32_t)b * 2654435761u) >> 22;
+                    if (s_seen[h] != b) acc += (unsigned long long)cta_first(s_seen, b);
+                } else {
+                    acc += (unsigned long long)b;
+                }
+            }
+        }
+    }
+    if (acc == 0x123456789ull) sink[0] = acc;
+    if (lane == 0) g_t[1][tw] = gtimer();
 }
 
 int main() {
@@ -146,17 +211,40 @@ int main() {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    const char* names[] = {"KA1 match/hash (r01)", "KA1 plain-load hash (r02)", "KA2 plain-load hash",
-                           "KA4 plain-load hash", "KA1 no hash", "KA2 no hash"};
-    const int fl[] = {7, 1 | 2 | 16, 1 | 2 | 16, 1 | 2 | 16, 3, 3};
-    const int ka[] = {1, 1, 2, 4, 1, 2};
-    for (int v = 0; v < 6; ++v) {
+    struct V { const char* name; int flags, ka; };
+    const V vs[] = {{"empty launch (g=0)", -1, 1},
+                    {"KA1 plain-load hash (r02)", 1 | 2 | 16, 1},
+                    {"KA4 plain-load hash", 1 | 2 | 16, 4},
+                    {"KA8 plain-load hash", 1 | 2 | 16, 8},
+                    {"KA4 rev only", 0, 4},
+                    {"KA4 rev + mark", 1, 4},
+                    {"KA4 rev + block", 2, 4},
+                    {"KA4 rev + block + mark", 3, 4},
+                    {"KA8 rev only", 0, 8},
+                    {"KA4 full + member prefetch", 1 | 2 | 16, 104},
+                    {"KA8 full + member prefetch", 1 | 2 | 16, 108},
+                    {"KA4 full, gathers before marks", 1 | 2 | 16 | 32, 4},
+                    {"KA8 full, gathers before marks", 1 | 2 | 16 | 32, 8},
+                    {"KA4 rev+block+mark, gathers first", 1 | 2 | 32, 4},
+                    {"KA4 full, gathers first + mprefetch", 1 | 2 | 16 | 32, 104},
+                    {"lane/member E4 full", 1 | 2 | 16, 204},
+                    {"lane/member E8 full", 1 | 2 | 16, 208},
+                    {"lane/member E12 full", 1 | 2 | 16, 212},
+                    {"lane/member E8 rev only", 0, 208}};
+    for (const V& v : vs) {
         int rep = 0;
         auto launch = [&]() {
             const int4* m = d_mem + (size_t)(rep++ % nset) * cz;
-            if (ka[v] == 1) walk<1><<<sms, 512>>>(m, cz, d_rev, d_blk, d_mark, d_markb, fl[v], d_sink);
-            else if (ka[v] == 2) walk<2><<<sms, 512>>>(m, cz, d_rev, d_blk, d_mark, d_markb, fl[v], d_sink);
-            else walk<4><<<sms, 512>>>(m, cz, d_rev, d_blk, d_mark, d_markb, fl[v], d_sink);
+            const int32_t z = v.flags < 0 ? 0 : cz;
+            const int f = v.flags < 0 ? 0 : v.flags;
+            if (v.ka == 1) walk<1><<<sms, 512>>>(m, z, d_rev, d_blk, d_mark, d_markb, f, d_sink);
+            else if (v.ka == 4) walk<4><<<sms, 512>>>(m, z, d_rev, d_blk, d_mark, d_markb, f, d_sink);
+            else if (v.ka == 8) walk<8><<<sms, 512>>>(m, z, d_rev, d_blk, d_mark, d_markb, f, d_sink);
+            else if (v.ka == 204) walk_lane<4><<<sms, 512>>>(m, z, d_rev, d_blk, d_mark, f, d_sink);
+            else if (v.ka == 208) walk_lane<8><<<sms, 512>>>(m, z, d_rev, d_blk, d_mark, f, d_sink);
+            else if (v.ka == 212) walk_lane<12><<<sms, 512>>>(m, z, d_rev, d_blk, d_mark, f, d_sink);
+            else if (v.ka == 104) walk<4, true><<<sms, 512>>>(m, z, d_rev, d_blk, d_mark, d_markb, f, d_sink);
+            else walk<8, true><<<sms, 512>>>(m, z, d_rev, d_blk, d_mark, d_markb, f, d_sink);
         };
         for (int w = 0; w < 3; ++w) launch();
         const int R = 50;
@@ -166,7 +254,22 @@ int main() {
         cudaEventSynchronize(e1);
         float ms;
         cudaEventElapsedTime(&ms, e0, e1);
-        printf("%-40s %7.2f us per walk (%s)\n", names[v], ms * 1e3 / R, cudaGetErrorString(cudaGetLastError()));
+        std::vector<unsigned long long> t(2 * 148 * 16);
+        cudaMemcpyFromSymbol(t.data(), g_t, t.size() * 8);
+        const int nw = sms * 16;
+        unsigned long long t0 = ~0ull;
+        for (int w = 0; w < nw; ++w) t0 = std::min(t0, t[w]);
+        std::vector<double> st, en;
+        for (int w = 0; w < nw; ++w) {
+            st.push_back((t[w] - t0) * 1e-3);
+            en.push_back((t[nw + w] - t0) * 1e-3);
+        }
+        std::sort(st.begin(), st.end());
+        std::sort(en.begin(), en.end());
+        auto q = [&](std::vector<double>& v, double f) { return v[std::min((size_t)(f * v.size()), v.size() - 1)]; };
+        printf("%-40s %7.2f us per walk (%s)  warp start p50/max %.2f/%.2f  end p10/p50/p90/p99/max %.2f/%.2f/%.2f/%.2f/%.2f\n",
+               v.name, ms * 1e3 / R, cudaGetErrorString(cudaGetLastError()), q(st, .5), st.back(), q(en, .1), q(en, .5),
+               q(en, .9), q(en, .99), en.back());
     }
     return 0;
 }
