@@ -89,6 +89,9 @@ typedef int (*bisim_observer_fn)(int64_t iteration, const int32_t *block, int32_
 #define BISIM_FLAG_NO_SOLO 2u              /* every round on the whole grid (no CTA-solo stretches) */
 #define BISIM_FLAG_CTA_MAJOR 4u            /* phase-B work items CTA-major */
 #define BISIM_FLAG_LITERAL_LABEL_ROUNDS 8u /* label pre-partition as |Act| literal rounds */
+#define BISIM_FLAG_WIDE_LAYOUT 16u         /* phase B: 128-member chunks even for small touched blocks */
+#define BISIM_FLAG_TWO_PASS 32u            /* phase B: the two-pass (tag, grid barrier, compact) split */
+#define BISIM_FLAG_BATCH_WALK 64u          /* phase A: batch registration wave for every grid splitter */
 
 typedef struct bisim_options {
     int32_t device;          /* CUDA ordinal */

@@ -24,6 +24,7 @@ DEFAULT_GUARD = -(2 ** 63)
 MODE_AUTO, MODE_PERSISTENT, MODE_STEPPED, MODE_DENSE = 0, 1, 2, 3
 # schedule variants (bisim.h BISIM_FLAG_*): none changes a result
 FLAG_NO_SKIP, FLAG_NO_SOLO, FLAG_CTA_MAJOR, FLAG_LITERAL_LABEL_ROUNDS = 1, 2, 4, 8
+FLAG_WIDE_LAYOUT, FLAG_TWO_PASS, FLAG_BATCH_WALK = 16, 32, 64
 
 i32p = ctypes.POINTER(ctypes.c_int32)
 OBSERVER = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_int64, i32p, ctypes.c_int32, ctypes.c_void_p)

@@ -834,7 +834,10 @@ int run_with(Ctx& c, Job& j) {
         sp.allow_solo = (j.opt.flags & BISIM_FLAG_NO_SOLO) ? 0 : 1;
         // developer: BISIM_MODE_B=1|2 forces the wide / two-pass phase-B layout
         sp.force_mode_b = dev_env("BISIM_MODE_B") ? atoi(dev_env("BISIM_MODE_B")) : -1;
+        if (j.opt.flags & BISIM_FLAG_WIDE_LAYOUT) sp.force_mode_b = std::max(sp.force_mode_b, 1);
+        if (j.opt.flags & BISIM_FLAG_TWO_PASS) sp.force_mode_b = 2;
         sp.batch_min_c = dev_env("BISIM_BATCH_C") ? atoi(dev_env("BISIM_BATCH_C")) : 8192;
+        if (j.opt.flags & BISIM_FLAG_BATCH_WALK) sp.batch_min_c = 1;
         sp.onepass_major = dev_env("BISIM_ONEPASS_MINOR") != nullptr ? 0
                            : dev_env("BISIM_MAJOR") ? atoi(dev_env("BISIM_MAJOR")) : kSparseThreads / 32;
         sp.wide_major = dev_env("BISIM_WIDE_MAJOR") ? atoi(dev_env("BISIM_WIDE_MAJOR")) : 0;

@@ -331,7 +331,9 @@ def test_noop_round_retirement_is_exact(mode):
 
 
 @pytest.mark.parametrize("flag", ["FLAG_NO_SOLO", "FLAG_NO_SKIP", "FLAG_CTA_MAJOR",
-                                  "FLAG_NO_SOLO|FLAG_NO_SKIP"])
+                                  "FLAG_NO_SOLO|FLAG_NO_SKIP", "FLAG_WIDE_LAYOUT|FLAG_NO_SOLO",
+                                  "FLAG_TWO_PASS|FLAG_NO_SOLO", "FLAG_BATCH_WALK|FLAG_NO_SOLO",
+                                  "FLAG_TWO_PASS|FLAG_BATCH_WALK|FLAG_NO_SOLO|FLAG_NO_SKIP"])
 def test_loop_variants_identical(flag):
     """Solo stretches, no-op retirement and work placement never change a
     result: every variant reproduces the oracle on mixed workloads."""

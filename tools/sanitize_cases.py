@@ -26,7 +26,8 @@ from paper_2105_11788_b200.post import is_stable_arrays, quotient_arrays  # noqa
 from paper_2105_11788_b200.sharded import bcrp_sharded_arrays  # noqa: E402
 
 FLAGS = [0, N.FLAG_NO_SKIP, N.FLAG_NO_SOLO, N.FLAG_NO_SOLO | N.FLAG_NO_SKIP, N.FLAG_CTA_MAJOR,
-         N.FLAG_LITERAL_LABEL_ROUNDS]
+         N.FLAG_LITERAL_LABEL_ROUNDS, N.FLAG_TWO_PASS | N.FLAG_NO_SOLO | N.FLAG_BATCH_WALK,
+         N.FLAG_WIDE_LAYOUT | N.FLAG_NO_SOLO]
 
 
 def check_bcrp(name):
