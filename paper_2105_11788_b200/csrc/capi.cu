@@ -820,11 +820,10 @@ int run_with(Ctx& c, Job& j) {
         sp.big_info = (int2*)c.big_info.ensure(((int64_t)n / 32 + 2) * 8);
         sp.big_info4 = (int2*)c.big_info4.ensure(((int64_t)n / 32 + 2) * 8);
         sp.tmp = (MemberRec*)c.tmp.ensure((int64_t)n * sizeof(MemberRec));
+        sp.srec = (SplitRec*)c.sarr.ensure((int64_t)n * sizeof(SplitRec));
         sp.scnt = (int32_t*)c.scnt.ensure((int64_t)n * 4);
-        sp.smin = (int32_t*)c.smin.ensure((int64_t)n * 4);
         sp.kcur = (int32_t*)c.kcur.ensure((int64_t)n * 4);
         sp.scur = (int32_t*)c.scur.ensure((int64_t)n * 4);
-        sp.sarr = (unsigned long long*)c.sarr.ensure((int64_t)n * 8);
         sp.splits = splits;
         sp.ctrl = (SCtrl*)ctrl;
         sp.bar = (GridBarrier*)c.bar.ensure(sizeof(GridBarrier));

@@ -270,7 +270,7 @@ __device__ int32_t big_tag(const SparseParams& p, int32_t nbig, int32_t ci) {
     chunk_counts<K>(c, bal, kb, nsplit, nkeep, wmin);
     if (lane == 0 && nsplit) {
         red_add(&p.scnt[l], nsplit);
-        red_min(&p.smin[l], wmin);
+        red_min(&p.srec[l].smin, wmin);
     }
     return min(32 * K, bz - ci0);
 }
@@ -296,12 +296,12 @@ __device__ void big_split(const SparseParams& p, int cur, int64_t round, int32_t
         t.y &= 0x7fffffff;
         c.r[j] = t;
     }
-    const int32_t ns = p.scnt[l];
+    const int32_t ns = p.scnt[l];  // final after the grid barrier
     if (ns) {
         unsigned bal[K], kb[K];
         int32_t nsplit, nkeep, wmin;
         chunk_counts<K>(c, bal, kb, nsplit, nkeep, wmin);
-        const int32_t w = p.smin[l];
+        const int32_t w = p.srec[l].smin;
         chunk_compact<K>(p, l, bs, bz, ns, w, c, bal, kb, nsplit, nkeep);
         if (ci0 == 0 && lane == 0) finish_block(p, cur, round, C, l, bs, bz, ns, w);
     }
@@ -328,11 +328,6 @@ constexpr int kCntBits = 21;
 constexpr unsigned long long kCntMask = (1ull << kCntBits) - 1ull;
 constexpr int kArrShift = 2 * kCntBits;
 
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
 
 struct OnePassSlot {
     int32_t key;     // big-list index of the warp's block, -1 if none
@@ -422,23 +417,20 @@ __device__ int32_t big_onepass_cta(const SparseParams& p, int cur, int64_t round
         if (nch_b > cnt_cta) {  // the block spans CTAs: combine globally
             if (lane == 0) {
                 unsigned long long v = 0ull;
-                bool done = false;
                 if (wid == leader) {
                     // one acq_rel add on the block's packed word reserves the
                     // placement bases (kept members fill the range from the
                     // head, split members from the tail, so the bases do not
                     // depend on the block's split count), publishes the counts
                     // and arrives; the released minimum is visible with it
-                    if (tot_s) red_min(&p.smin[l], mn);
+                    if (tot_s) red_min(&p.srec[l].smin, mn);
                     const unsigned long long add = ((unsigned long long)cnt_cta << kArrShift) |
                                                    ((unsigned long long)tot_s << kCntBits) | (unsigned)tot_k;
                     unsigned long long old;
                     asm volatile("atom.add.acq_rel.gpu.global.u64 %0, [%1], %2;"
-                                 : "=l"(old) : "l"(&p.sarr[l]), "l"(add) : "memory");
+                                 : "=l"(old) : "l"(&p.srec[l].arr), "l"(add) : "memory");
                     slot[wid].sbase = (int32_t)((old >> kCntBits) & kCntMask);
                     slot[wid].kbase = (int32_t)(old & kCntMask);
-                    v = old + add;
-                    done = (int32_t)(v >> kArrShift) >= nch_b;  // the last arrival waits for nobody
                 }
                 // only the CTA leader of the block polls the word; the
                 // CTA's other warps of the block read its result after the
@@ -448,12 +440,23 @@ __device__ int32_t big_onepass_cta(const SparseParams& p, int cur, int64_t round
 #else
                 if (wid == leader) {
 #endif
-                    while (!done) {
-                        v = ld_acquire_u64(&p.sarr[l]);
-                        done = (int32_t)(v >> kArrShift) >= nch_b;
-                    }
+                    // the record's arrival word and minimum in one 16-byte
+                    // acquire load (the last arriver's first load sees both)
+                    int32_t mw = kBig;
+                    do {
+                        unsigned w0, w1, w2, w3;
+                        asm volatile(
+                            "{\n\t.reg .b128 t;\n\tld.acquire.gpu.global.b128 t, [%4];\n\t"
+                            "mov.b128 {%0, %1, %2, %3}, t;\n\t}"
+                            : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
+                            : "l"(&p.srec[l])
+                            : "memory");
+                        (void)w3;
+                        v = ((unsigned long long)w1 << 32) | w0;
+                        mw = (int32_t)w2;
+                    } while ((int32_t)(v >> kArrShift) < nch_b);
                     ns = (int32_t)((v >> kCntBits) & kCntMask);
-                    w = ns ? ld_vol(&p.smin[l]) : kBig;
+                    w = ns ? mw : kBig;
                     if (wid == leader) {
                         slot[wid].ns = ns;
                         slot[wid].w = w;

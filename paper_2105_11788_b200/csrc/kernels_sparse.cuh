@@ -151,6 +151,18 @@ constexpr int32_t kSkipMaxEdges = 256;
 #endif
 constexpr int kWide = BISIM_KWIDE;  // members per lane in the wide big-block chunk layout (kernels_big.cuh)
 
+// Per-label split record of a big touched block, 16 bytes: the one-pass
+// packed arrival word (kernels_big.cuh) and the new-leader minimum
+// (red.min).  A one-pass poller reads
+// arrival word and minimum with ONE 16-byte acquire load: the arrivals'
+// release orders each CTA's red.min before its add, so the load that sees
+// the last arrival carries the final minimum (no dependent load after it).
+struct alignas(16) SplitRec {
+    unsigned long long arr;
+    int32_t smin;
+    int32_t pad;
+};
+
 // A member record carries what the phases read right after the member id,
 // so one 16-byte load replaces two dependent ones: (state u, slot base
 // off[u] (BCRP; unused for RCPP), in-edge range [e0, e1) of u in the
@@ -187,11 +199,11 @@ struct SparseParams {
     int2* big_info;       // leader slot base / slot count of each big_list entry
     int2* big_info4;      // same for big_list4
     int4* tmp;            // per member position: the record, x = -1-state if split
-    int32_t* scnt;        // per label: split count / min split / compaction cursors
-    int32_t* smin;
-    int32_t* kcur;
-    int32_t* scur;
-    unsigned long long* sarr;  // per label: packed arrival word of the one-pass split (kernels_big.cuh)
+    SplitRec* srec;       // per label: arrival word and new-leader minimum (kernels_big.cuh)
+    int32_t* scnt;        // per label: two-pass split count (its own line: the pass-1 reductions
+                          //   of a block's chunks would otherwise queue behind its minimum's)
+    int32_t* kcur;        // per label: two-pass compaction cursors, kept / split members (separate
+    int32_t* scur;        //   arrays: a chunk's two returning atomics must not queue on one line)
     int32_t* splits;
     SCtrl* ctrl;
     GridBarrier* bar;
@@ -495,11 +507,14 @@ __device__ __forceinline__ void register_blocks_warp(const SparseParams& p, int 
         p.big_list4[k4] = make_int4(b, r.x, r.y, base4);
         p.big_base4[k4] = base4;
         p.big_info4[k4] = make_int2(ob, nb);
+        SplitRec z;
+        z.arr = 0ull;
+        z.smin = kBig;
+        z.pad = 0;
+        p.srec[b] = z;
         p.scnt[b] = 0;
-        p.smin[b] = kBig;
         p.kcur[b] = 0;
         p.scur[b] = 0;
-        p.sarr[b] = 0ull;
     }
 }
 

@@ -94,6 +94,13 @@ __global__ void __launch_bounds__(512, 1) walk(const int4* members, int32_t cz, 
             int32_t bb[KA];
 #pragma unroll
             for (int u = 0; u < KA; ++u) {
+                if (flags & 64) {  // per-state record (block | mark bits << 32): one returning atomic
+                    bb[u] = act[u] ? (int32_t)atomicOr((unsigned long long*)markb + rv[u].y,
+                                                       1ull << (32 + (rv[u].x & 31)))
+                                   : 0;
+                    continue;
+                }
+                if ((flags & 8) && act[u]) markb[rv[u].x] = 1;  // byte map: a plain store, no L2 atomic
                 if (!(flags & 32) && act[u] && (flags & 1)) red_or(&mark[rv[u].x >> 5], 1u << (rv[u].x & 31));
                 bb[u] = (act[u] && (flags & 2)) ? block[rv[u].y] : rv[u].y;
             }
@@ -199,13 +206,17 @@ int main() {
     cudaMalloc(&d_rev, rev.size() * 8);
     cudaMalloc(&d_blk, (size_t)n * 4);
     cudaMalloc(&d_mark, (size_t)5 * n / 8 + 64);
-    cudaMalloc(&d_markb, (size_t)5 * n + 64);
+    cudaMalloc(&d_markb, (size_t)8 * n + 64);
     cudaMalloc(&d_sink, 8);
     cudaMemcpy(d_mem, mem.data(), mem.size() * 16, cudaMemcpyHostToDevice);
     cudaMemcpy(d_rev, rev.data(), rev.size() * 8, cudaMemcpyHostToDevice);
     cudaMemcpy(d_blk, blk.data(), (size_t)n * 4, cudaMemcpyHostToDevice);
     cudaMemset(d_mark, 0, (size_t)5 * n / 8 + 64);
-    cudaMemset(d_markb, 0, (size_t)5 * n + 64);
+    {
+        std::vector<unsigned long long> rec(n);
+        for (int32_t i = 0; i < n; ++i) rec[i] = (uint32_t)blk[i];
+        cudaMemcpy(d_markb, rec.data(), (size_t)8 * n, cudaMemcpyHostToDevice);
+    }
     int sms;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     cudaEvent_t e0, e1;
@@ -230,7 +241,13 @@ int main() {
                     {"lane/member E4 full", 1 | 2 | 16, 204},
                     {"lane/member E8 full", 1 | 2 | 16, 208},
                     {"lane/member E12 full", 1 | 2 | 16, 212},
-                    {"lane/member E8 rev only", 0, 208}};
+                    {"lane/member E8 rev only", 0, 208},
+                    {"KA4 rec64 atomic + hash", 64 | 16, 4},
+                    {"KA4 rec64 atomic, no hash", 64, 4},
+                    {"KA8 rec64 atomic + hash", 64 | 16, 8},
+                    {"KA4 byte-map store + block + hash", 8 | 2 | 16, 4},
+                    {"KA4 byte-map store + block", 8 | 2, 4},
+                    {"KA4 rev + mark + hash (no block)", 1 | 16, 4}};
     for (const V& v : vs) {
         int rep = 0;
         auto launch = [&]() {
