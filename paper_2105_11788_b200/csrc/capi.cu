@@ -545,12 +545,12 @@ int run_with(Ctx& c, Job& j) {
     int32_t* bcur = dense ? nullptr : (int32_t*)c.bcur.ensure((int64_t)nb * 4);
     int4* stage = dense ? nullptr : (int4*)c.stage.ensure(mm * 16);
     auto bucket_pass = [&](int64_t len, const int32_t* s_, const int32_t* a_, const int32_t* d_, int32_t lo,
-                           int32_t hi, bool slot_here, const int4* si) {
+                           int32_t hi, bool slot_here, const int4* si, const int2* si2) {
         if (len <= 0) return;
         const int64_t tiles = (len + kBucketTile - 1) / kBucketTile;
         const int g1 = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)c.sms * 4));
         k_rev_bucket<<<g1, kBucketThreads, 0, st>>>(len, s_, a_, d_, shift, nb, bcur, stage, lo, hi, slot_here, n,
-                                                    si, lmask, off);
+                                                    si, lmask, off, si2);
         ++c.launches;
     };
     auto rev_ptr_scan = [&]() {
@@ -605,7 +605,7 @@ int run_with(Ctx& c, Job& j) {
             CK(cudaStreamWaitEvent(st, pev[2 + k], 0));
             k_label_mask<<<grid_for(len, TB, c.sms), TB, 0, st>>>(n, len, A, ds + i0, da + i0, dd + i0, lmask, ctrl);
             ++c.launches;
-            bucket_pass(len, ds + i0, da + i0, dd + i0, 0, n, false, nullptr);  // (t, s, action)
+            bucket_pass(len, ds + i0, da + i0, dd + i0, 0, n, false, nullptr, nullptr);  // (t, s, action)
         }
     } else {
         if (j.inputs_on_device) {
@@ -653,11 +653,16 @@ int run_with(Ctx& c, Job& j) {
                                                 : "edge outside 0..n-1 or pi0 is not a leader-form partition");
     }
     int4* sinfo = nullptr;
+    int2* sinfo2 = nullptr;
     if (j.bcrp) {
         k_nr_marks<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, W, lmask, off);
         ++c.launches;
         scan_excl(c, off, n);
-        if (W == 1 && !dense) {
+        if (A <= 32 && !dense) {
+            sinfo2 = (int2*)c.sinfo.ensure((int64_t)n * 8);
+            k_pack_sinfo2<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, lmask, off, sinfo2);
+            ++c.launches;
+        } else if (W == 1 && !dense) {
             sinfo = (int4*)c.sinfo.ensure((int64_t)n * 16);
             k_pack_sinfo<<<grid_for(n, TB, c.sms), TB, 0, st>>>(n, lmask, off, sinfo);
             ++c.launches;
@@ -673,7 +678,7 @@ int run_with(Ctx& c, Job& j) {
             ++c.launches;
         }
         rev_ptr_scan();
-        if (!dense) bucket_pass(m, d_src, d_act, d_dst, src_lo, src_hi, slot_staged, sinfo);
+        if (!dense) bucket_pass(m, d_src, d_act, d_dst, src_lo, src_hi, slot_staged, sinfo, sinfo2);
     }
     if (m) {
         if (dense) {
@@ -698,10 +703,10 @@ int run_with(Ctx& c, Job& j) {
                                                               nullptr, nullptr);
             else if (slot_staged)
                 k_rev_place<true, true><<<g2, 256, 0, st>>>(rev_ptr + n, stage, cursor, rev2, nullptr, n, lmask, off,
-                                                            sinfo);
+                                                            sinfo, sinfo2);
             else
                 k_rev_place<true, false><<<g2, 256, 0, st>>>(rev_ptr + n, stage, cursor, rev2, nullptr, n, lmask,
-                                                             off, sinfo);
+                                                             off, sinfo, sinfo2);
         }
         ++c.launches;
     }

@@ -799,6 +799,26 @@ __global__ void k_pack_sinfo(int32_t n, const unsigned long long* __restrict__ l
     }
 }
 
+// |Act| <= 32: (label mask, slot base) in 8 bytes -- half the footprint of
+// the random lookups (c5: 80 MB instead of 160 MB, mostly L2 hits).
+__global__ void k_pack_sinfo2(int32_t n, const unsigned long long* __restrict__ lmask,
+                              const int32_t* __restrict__ off, int2* sinfo2) {
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x)
+        sinfo2[s] = make_int2((int32_t)(uint32_t)lmask[s], off[s]);
+}
+
+// mark slot of (source s, action a) from a packed record (bcrp.py:219)
+__device__ __forceinline__ int32_t slot_of(int32_t s, int32_t a, const int4* __restrict__ sinfo,
+                                           const int2* __restrict__ sinfo2) {
+    if (sinfo2) {
+        const int2 q = sinfo2[s];
+        return q.y + __popc((uint32_t)q.x & ((1u << (a & 31)) - 1u));
+    }
+    const int4 q = sinfo[s];
+    const unsigned long long w = ((unsigned long long)(uint32_t)q.y << 32) | (uint32_t)q.x;
+    return q.z + __popcll(w & ((1ull << (a & 63)) - 1ull));
+}
+
 // Pack BCRP reverse edges (slot, source) for one 8-byte load per in-edge.
 template <bool BCRP>
 __global__ void k_rev_fill2(int32_t n, int64_t m, const int32_t* __restrict__ src,
@@ -854,7 +874,10 @@ __global__ void k_rev_fill2(int32_t n, int64_t m, const int32_t* __restrict__ sr
 // positions it scatters to lie in the one or two buckets being worked on --
 // a few MB that stay in L2 until their sectors are complete.
 constexpr int kBucketThreads = 512;
-constexpr int kBucketItems = 8;                        // transitions per thread per tile
+#ifndef BISIM_BUCKET_ITEMS
+#define BISIM_BUCKET_ITEMS 8
+#endif
+constexpr int kBucketItems = BISIM_BUCKET_ITEMS;                        // transitions per thread per tile
 constexpr int kBucketTile = kBucketThreads * kBucketItems;
 constexpr int kMaxBuckets = 1024;
 
@@ -876,7 +899,8 @@ __global__ void __launch_bounds__(kBucketThreads) k_rev_bucket(
     int64_t m, const int32_t* __restrict__ src, const int32_t* __restrict__ act,
     const int32_t* __restrict__ dst, int shift, int32_t nb, int32_t* bcur, int4* stage, int32_t lo, int32_t hi,
     bool slot_here = false, int32_t n = 0, const int4* __restrict__ sinfo = nullptr,
-    const unsigned long long* __restrict__ lmask = nullptr, const int32_t* __restrict__ off = nullptr) {
+    const unsigned long long* __restrict__ lmask = nullptr, const int32_t* __restrict__ off = nullptr,
+    const int2* __restrict__ sinfo2 = nullptr) {
     __shared__ int32_t cnt[kMaxBuckets];
     __shared__ int32_t base[kMaxBuckets];
     for (int64_t t0 = (int64_t)blockIdx.x * kBucketTile; t0 < m; t0 += (int64_t)gridDim.x * kBucketTile) {
@@ -899,10 +923,8 @@ __global__ void __launch_bounds__(kBucketThreads) k_rev_bucket(
         for (int k = 0; k < kBucketItems; ++k) {
             if (t[k] < 0) continue;
             if (slot_here) {  // a[k] := the mark slot (bcrp.py:219)
-                if (sinfo) {
-                    const int4 q = sinfo[s[k]];
-                    const unsigned long long w = ((unsigned long long)(uint32_t)q.y << 32) | (uint32_t)q.x;
-                    a[k] = q.z + __popcll(w & ((1ull << (a[k] & 63)) - 1ull));
+                if (sinfo || sinfo2) {
+                    a[k] = slot_of(s[k], a[k], sinfo, sinfo2);
                 } else {
                     a[k] = off[s[k]] + label_rank(lmask, n, s[k], a[k]);
                 }
@@ -949,7 +971,8 @@ __global__ void k_indeg_checked(int32_t n, int64_t m, const int32_t* __restrict_
 template <bool BCRP, bool SLOT>
 __global__ void k_rev_place(const int32_t* __restrict__ ptotal, const int4* __restrict__ stage, int32_t* cursor,
                             int2* rev, int32_t* rev_src, int32_t n, const unsigned long long* __restrict__ lmask,
-                            const int32_t* __restrict__ off, const int4* __restrict__ sinfo) {
+                            const int32_t* __restrict__ off, const int4* __restrict__ sinfo,
+                            const int2* __restrict__ sinfo2 = nullptr) {
     const int lane = threadIdx.x & 31;
     const int64_t total = *ptotal;
     for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < total;
@@ -967,10 +990,8 @@ __global__ void k_rev_place(const int32_t* __restrict__ ptotal, const int4* __re
                 int32_t slot;
                 if (SLOT) {
                     slot = a;
-                } else if (sinfo) {
-                    const int4 si = sinfo[sv];
-                    const unsigned long long w = ((unsigned long long)(uint32_t)si.y << 32) | (uint32_t)si.x;
-                    slot = si.z + __popcll(w & ((1ull << (a & 63)) - 1ull));
+                } else if (sinfo || sinfo2) {
+                    slot = slot_of(sv, a, sinfo, sinfo2);
                 } else {
                     slot = off[sv] + label_rank(lmask, n, sv, a);
                 }
