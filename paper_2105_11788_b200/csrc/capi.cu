@@ -16,6 +16,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <atomic>
 #include <thread>
 #include <vector>
 
@@ -72,8 +73,10 @@ struct Ctx {
     std::mutex mu;
     DevBuf src, act, dst, pi0, lmask, off, rev_ptr, cursor, rev_slot, block, nl, mark, unstable,
         split_list, cmem, splits, ctrl, scan_tmp, rev2, members, bstart, bsize, tblock,
-        small_list, big_list, big_base, tmp, scnt, smin, kcur, scur, counter, brange, bar, trace, lhash, lkeys,
-        lmins, sarr, big_list4, big_base4, big_info, big_info4, sinfo, nrm, bcur, stage;
+        small_list, big_list, big_base, tmp, scnt, kcur, scur, counter, brange, bar, trace, lhash, lkeys,
+        lmins, sarr, big_list4, big_base4, big_info, big_info4, sinfo, nrm, bcur, stage, act8;
+    uint8_t* act8_host = nullptr;     // pinned: host actions narrowed to bytes (pipelined input path)
+    size_t act8_cap = 0;
     int launches = 0;
     struct Stager* stager = nullptr;  // pinned staging of pageable host arrays (lazy)
     cudaStream_t cstream = nullptr;   // host-to-device copies overlapping preprocessing
@@ -177,6 +180,7 @@ Ctx::~Ctx() {
     for (auto& e : ev)
         if (e) cudaEventDestroy(e);
     for (auto e : pev) cudaEventDestroy(e);
+    if (act8_host) cudaFreeHost(act8_host);
     if (cstream) cudaStreamDestroy(cstream);
     if (stream) cudaStreamDestroy(stream);
 }
@@ -480,6 +484,70 @@ cudaEvent_t* pipe_events(Ctx& c) {
     return c.pev.data();
 }
 
+// Host threads narrowing the caller's int32 actions to bytes in the
+// context's pinned buffer, chunk by chunk in order (the pipelined input path
+// DMAs chunk k as soon as its slices are done).
+struct ActPacker {
+    static constexpr int kSlices = 8;  // work units per chunk
+    std::vector<std::thread> th;
+    std::atomic<int> next{0};
+    std::atomic<int> done[kPipeChunks];
+    std::atomic<bool> bad_flag{false};
+    bool bad = false;
+    int64_t m = 0, chunk = 0;
+    ActPacker() {
+        for (auto& d : done) d.store(0);
+    }
+    void start(Ctx& c, const int32_t* act, int64_t m_, int64_t chunk_) {
+        m = m_;
+        chunk = chunk_;
+        if (c.act8_cap < (size_t)m) {
+            if (c.act8_host) CK(cudaFreeHost(c.act8_host));
+            c.act8_host = nullptr;
+            c.act8_cap = 0;
+            CK(cudaHostAlloc((void**)&c.act8_host, (size_t)m, cudaHostAllocPortable));
+            c.act8_cap = (size_t)m;
+        }
+        uint8_t* out = c.act8_host;
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        int T = (int)std::max(1u, std::min(8u, hw / 2));
+        if (const char* e = dev_env("BISIM_PACK_THREADS")) T = std::max(1, atoi(e));
+        for (int t = 0; t < T; ++t)
+            th.emplace_back([this, act, out] {
+                bool b = false;
+                for (;;) {
+                    const int u = next.fetch_add(1, std::memory_order_relaxed);
+                    if (u >= kPipeChunks * kSlices) break;
+                    const int k = u / kSlices, q = u % kSlices;
+                    const int64_t c0 = k * chunk, c1 = std::min<int64_t>(c0 + chunk, m);
+                    const int64_t per = (chunk + kSlices - 1) / kSlices;
+                    const int64_t lo = std::min<int64_t>(c0 + q * per, c1), hi = std::min<int64_t>(lo + per, c1);
+                    uint32_t any = 0;
+                    for (int64_t i = lo; i < hi; ++i) {
+                        const uint32_t v = (uint32_t)act[i];
+                        any |= v;
+                        out[i] = (uint8_t)v;
+                    }
+                    b |= (any >> 8) != 0;  // some action outside 0..255
+                    done[k].fetch_add(1, std::memory_order_release);
+                }
+                if (b) bad_flag.store(true);
+            });
+    }
+    void wait(int k) {
+        while (done[k].load(std::memory_order_acquire) < kSlices) std::this_thread::yield();
+    }
+    void join() {
+        for (auto& t : th) t.join();
+        th.clear();
+        bad = bad_flag.load();
+    }
+    ~ActPacker() {
+        for (auto& t : th)
+            if (t.joinable()) t.join();
+    }
+};
+
 int run_with(Ctx& c, Job& j);
 
 int run(Job& j) { return run_with(*get_ctx(j.opt.device), j); }
@@ -544,7 +612,7 @@ int run_with(Ctx& c, Job& j) {
     const int32_t nb = (int32_t)(((int64_t)n - 1) >> shift) + 1;
     int32_t* bcur = dense ? nullptr : (int32_t*)c.bcur.ensure((int64_t)nb * 4);
     int4* stage = dense ? nullptr : (int4*)c.stage.ensure(mm * 16);
-    auto bucket_pass = [&](int64_t len, const int32_t* s_, const int32_t* a_, const int32_t* d_, int32_t lo,
+    auto bucket_pass = [&](int64_t len, const int32_t* s_, auto a_, const int32_t* d_, int32_t lo,
                            int32_t hi, bool slot_here, const int4* si, const int2* si2) {
         if (len <= 0) return;
         const int64_t tiles = (len + kBucketTile - 1) / kBucketTile;
@@ -573,6 +641,7 @@ int run_with(Ctx& c, Job& j) {
     // chunks already on the device; dst goes first, its in-degrees fix the
     // bucket layout.
     const bool pipe = j.bcrp && !j.inputs_on_device && !sharded && !dense && m >= kPipeMin;
+    bool host_bad = false;  // the host narrowing of the actions met one outside 0..255
     CK(cudaEventRecord(c.ev[0], st));
     CK(cudaMemsetAsync(ctrl, 0, std::max(sizeof(Ctrl), sizeof(SCtrl)), st));
     CK(cudaMemsetAsync(rev_ptr, 0, ((int64_t)n + 1) * 4, st));
@@ -596,16 +665,41 @@ int run_with(Ctx& c, Job& j) {
         ++c.launches;
         rev_ptr_scan();
         const int64_t chunk = (m + kPipeChunks - 1) / kPipeChunks;
+        // |Act| <= 256: host threads narrow the actions to bytes in pinned
+        // memory, chunk by chunk ahead of the DMA, so a quarter of their
+        // bytes cross PCIe (an action outside 0..255 is flagged here, one in
+        // A..255 by k_label_mask, as before)
+        const bool narrow = A <= 256 && !dev_env("BISIM_NO_NARROW");
+        ActPacker pk;
+        if (narrow) pk.start(c, j.act, m, chunk);
+        uint8_t* da8 = narrow ? (uint8_t*)c.act8.ensure(mm) : nullptr;
         for (int k = 0; k < kPipeChunks; ++k) {
             const int64_t i0 = k * chunk, len = std::min<int64_t>(chunk, m - i0);
             if (len <= 0) break;
             h2d(c, ds + i0, j.src + i0, len * 4, cs);
-            h2d(c, da + i0, j.act + i0, len * 4, cs);
+            if (narrow) {
+                pk.wait(k);
+                CK(cudaMemcpyAsync(da8 + i0, c.act8_host + i0, len, cudaMemcpyHostToDevice, cs));
+            } else {
+                h2d(c, da + i0, j.act + i0, len * 4, cs);
+            }
             CK(cudaEventRecord(pev[2 + k], cs));
             CK(cudaStreamWaitEvent(st, pev[2 + k], 0));
-            k_label_mask<<<grid_for(len, TB, c.sms), TB, 0, st>>>(n, len, A, ds + i0, da + i0, dd + i0, lmask, ctrl);
-            ++c.launches;
-            bucket_pass(len, ds + i0, da + i0, dd + i0, 0, n, false, nullptr, nullptr);  // (t, s, action)
+            if (narrow) {
+                k_label_mask<<<grid_for(len, TB, c.sms), TB, 0, st>>>(n, len, A, ds + i0, (const uint8_t*)da8 + i0,
+                                                                      dd + i0, lmask, ctrl);
+                ++c.launches;
+                bucket_pass(len, ds + i0, (const uint8_t*)da8 + i0, dd + i0, 0, n, false, nullptr, nullptr);
+            } else {
+                k_label_mask<<<grid_for(len, TB, c.sms), TB, 0, st>>>(n, len, A, ds + i0, (const int32_t*)da + i0,
+                                                                      dd + i0, lmask, ctrl);
+                ++c.launches;
+                bucket_pass(len, ds + i0, (const int32_t*)da + i0, dd + i0, 0, n, false, nullptr, nullptr);
+            }
+        }
+        if (narrow) {
+            pk.join();
+            if (pk.bad) host_bad = true;
         }
     } else {
         if (j.inputs_on_device) {
@@ -648,7 +742,7 @@ int run_with(Ctx& c, Job& j) {
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(&bad, &ctrl->bad, sizeof(bad), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        if (bad)
+        if (bad || host_bad)
             throw Error(BISIM_BAD_INPUT, j.bcrp ? "transition mentions a state or action outside range"
                                                 : "edge outside 0..n-1 or pi0 is not a leader-form partition");
     }

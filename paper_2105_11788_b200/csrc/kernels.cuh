@@ -172,8 +172,10 @@ __device__ __forceinline__ unsigned long long run_or(unsigned long long v, const
     return v;
 }
 
+// TA: int32_t, or uint8_t for actions narrowed on the host (|Act| <= 256)
+template <typename TA = int32_t>
 __global__ void k_label_mask(int32_t n, int64_t m, int32_t A, const int32_t* __restrict__ src,
-                             const int32_t* __restrict__ act, const int32_t* __restrict__ dst,
+                             const TA* __restrict__ act, const int32_t* __restrict__ dst,
                              unsigned long long* lmask, Ctrl* ctrl) {
     const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -182,7 +184,7 @@ __global__ void k_label_mask(int32_t n, int64_t m, int32_t A, const int32_t* __r
         bool ok = false;
         unsigned long long addr = ~0ull - lane, bits = 0;
         if (i < m) {
-            const int32_t s = src[i], a = act[i], t = dst[i];
+            const int32_t s = src[i], a = (int32_t)act[i], t = dst[i];
             ok = (unsigned)s < (unsigned)n && (unsigned)t < (unsigned)n && (unsigned)a < (unsigned)A;
             if (ok) {
                 addr = (unsigned long long)(a >> 6) * n + s;

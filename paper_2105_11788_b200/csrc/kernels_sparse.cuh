@@ -895,8 +895,9 @@ __global__ void k_bucket_init(int32_t n, int shift, int32_t nb, const int32_t* _
 // slot_here (the label sets are complete): the mark slot is computed here
 // instead of the action, so pass 2 needs no per-source lookup (the random
 // label-set read overlaps the tile's other loads better here).
+template <typename TA = int32_t>
 __global__ void __launch_bounds__(kBucketThreads) k_rev_bucket(
-    int64_t m, const int32_t* __restrict__ src, const int32_t* __restrict__ act,
+    int64_t m, const int32_t* __restrict__ src, const TA* __restrict__ act,
     const int32_t* __restrict__ dst, int shift, int32_t nb, int32_t* bcur, int4* stage, int32_t lo, int32_t hi,
     bool slot_here = false, int32_t n = 0, const int4* __restrict__ sinfo = nullptr,
     const unsigned long long* __restrict__ lmask = nullptr, const int32_t* __restrict__ off = nullptr,
@@ -915,7 +916,7 @@ __global__ void __launch_bounds__(kBucketThreads) k_rev_bucket(
                 s[k] = src[i];
                 if (s[k] >= lo && s[k] < hi) {
                     t[k] = dst[i];
-                    a[k] = act ? act[i] : 0;
+                    a[k] = act ? (int32_t)act[i] : 0;
                 }
             }
         }

@@ -341,3 +341,37 @@ def test_c_abi_preprocess_per_original_transition(name):
     perm, sw, ref_order, ref_nr, ref_off, ref_L = oracle.preprocess(n, src, act, A)
     assert list(order[:m][perm]) == list(ref_order)
     assert list(nr) == list(ref_nr) and list(off) == list(ref_off) and L.value == ref_L
+
+
+@pytest.mark.parametrize("bad_act", [300, 256, -1, 40, 1 << 20])
+@pytest.mark.parametrize("pinned", [False, True])
+def test_out_of_range_actions_on_the_pipelined_input_path(bad_act, pinned):
+    """Host inputs of >= 4M transitions take the pipelined copy path, where
+    host threads narrow the actions to bytes (|Act| <= 256): an action
+    outside 0..255 is caught on the host, one in |Act|..255 on the device --
+    either way ValueError before anything scatters, and the device stays
+    usable; a valid system of that size still matches the oracle."""
+    from oracle import oracle
+    from paper_2105_11788_b200 import workloads as W
+    inst = W.c4_uniform(n=500_000, m=4_300_000, num_actions=40, seed=3)
+    act = inst.act.copy()
+    act[3_333_333] = bad_act
+    src, dst = inst.src, inst.dst
+    if pinned:  # the C ABI path a pinned caller takes (no staging threads)
+        import torch
+        src, act, dst = (torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy() for x in (src, act, dst))
+    with pytest.raises(ValueError):
+        bcrp_arrays(inst.n, src, act, dst, inst.num_actions)
+    block, st, _ = bcrp_arrays(inst.n, inst.src, inst.act, inst.dst, inst.num_actions)
+    res = _pipelined_oracle(inst)
+    assert np.array_equal(block, res.block)
+    assert st.supersteps == res.supersteps
+
+
+_PIPE_ORACLE = {}
+
+
+def _pipelined_oracle(inst):
+    if inst.name not in _PIPE_ORACLE:
+        _PIPE_ORACLE[inst.name] = oracle.bcrp_fast(inst.n, inst.src, inst.act, inst.dst, inst.num_actions)
+    return _PIPE_ORACLE[inst.name]
