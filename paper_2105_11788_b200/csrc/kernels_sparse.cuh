@@ -888,9 +888,9 @@ __global__ void k_bucket_init(int32_t n, int shift, int32_t nb, const int32_t* _
 
 // Pass 1 over transitions [0, m) of (src, act, dst) -- a chunk of the input
 // (the host path runs it per chunk while the next chunk is still being
-// copied): stage (target, source, action) by target bucket.  Targets were
-// validated before (k_indeg_checked); sources and actions may still be out
-// of range, which the caller detects (k_label_mask) before pass 2 uses them.
+// copied): stage (target, source, action) by target bucket.  Out-of-range
+// targets and sources are skipped (k_indeg_checked / k_label_mask flag
+// them, and the caller reads the flag before pass 2 uses anything).
 //
 // slot_here (the label sets are complete): the mark slot is computed here
 // instead of the action, so pass 2 needs no per-source lookup (the random
@@ -916,6 +916,10 @@ __global__ void __launch_bounds__(kBucketThreads) k_rev_bucket(
                 s[k] = src[i];
                 if (s[k] >= lo && s[k] < hi) {
                     t[k] = dst[i];
+                    // the pipelined input path buckets before the host reads
+                    // the validation flag back: an out-of-range target (flagged
+                    // by k_indeg_checked) must not index a bucket
+                    if ((unsigned)t[k] >= (unsigned)n) t[k] = -1;
                     a[k] = act ? (int32_t)act[i] : 0;
                 }
             }

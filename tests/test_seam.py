@@ -343,20 +343,23 @@ def test_c_abi_preprocess_per_original_transition(name):
     assert list(nr) == list(ref_nr) and list(off) == list(ref_off) and L.value == ref_L
 
 
-@pytest.mark.parametrize("bad_act", [300, 256, -1, 40, 1 << 20])
+@pytest.mark.parametrize("which,bad", [("act", 300), ("act", 256), ("act", -1), ("act", 40), ("act", 1 << 20),
+                                       ("dst", 500_000), ("dst", 1 << 24), ("dst", -1), ("dst", (1 << 24) + 7),
+                                       ("src", 500_000), ("src", 1 << 25), ("src", -5)])
 @pytest.mark.parametrize("pinned", [False, True])
-def test_out_of_range_actions_on_the_pipelined_input_path(bad_act, pinned):
-    """Host inputs of >= 4M transitions take the pipelined copy path, where
-    host threads narrow the actions to bytes (|Act| <= 256): an action
-    outside 0..255 is caught on the host, one in |Act|..255 on the device --
-    either way ValueError before anything scatters, and the device stays
-    usable; a valid system of that size still matches the oracle."""
-    from oracle import oracle
+def test_out_of_range_ids_on_the_pipelined_input_path(which, bad, pinned):
+    """Host inputs of >= 4M transitions take the pipelined copy path: the
+    chunks are bucketed before the validation flag is read back, and host
+    threads narrow the actions to bytes (|Act| <= 256).  An action that does
+    not fit a byte is caught on the host, any other out-of-range id on the
+    device -- either way ValueError before anything scatters through it, and
+    the device stays usable; a valid system of that size still matches the
+    oracle."""
     from paper_2105_11788_b200 import workloads as W
     inst = W.c4_uniform(n=500_000, m=4_300_000, num_actions=40, seed=3)
-    act = inst.act.copy()
-    act[3_333_333] = bad_act
-    src, dst = inst.src, inst.dst
+    arrs = {"src": inst.src.copy(), "act": inst.act.copy(), "dst": inst.dst.copy()}
+    arrs[which][3_333_333 if which != "dst" else 17] = bad
+    src, act, dst = arrs["src"], arrs["act"], arrs["dst"]
     if pinned:  # the C ABI path a pinned caller takes (no staging threads)
         import torch
         src, act, dst = (torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy() for x in (src, act, dst))
