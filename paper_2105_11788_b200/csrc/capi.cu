@@ -918,7 +918,10 @@ int run_with(Ctx& c, Job& j) {
         sp.big_base4 = (int32_t*)c.big_base4.ensure(((int64_t)n / 32 + 2) * 4);
         sp.big_info = (int2*)c.big_info.ensure(((int64_t)n / 32 + 2) * 8);
         sp.big_info4 = (int2*)c.big_info4.ensure(((int64_t)n / 32 + 2) * 8);
-        sp.tmp = (MemberRec*)c.tmp.ensure((int64_t)n * sizeof(MemberRec));
+        // chunk-major two-pass records: at most n / 128 + (blocks of > 32
+        // members < n / 32) chunks of 32 * kWide members
+        sp.tmp = (MemberRec*)c.tmp.ensure(((int64_t)n / (32 * kWide) + (int64_t)n / 32 + 2) * 32 * kWide *
+                                          (int64_t)sizeof(MemberRec));
         sp.srec = (SplitRec*)c.sarr.ensure((int64_t)n * sizeof(SplitRec));
         sp.scnt = (int32_t*)c.scnt.ensure((int64_t)n * 4);
         sp.kcur = (int32_t*)c.kcur.ensure((int64_t)n * 4);

@@ -263,7 +263,7 @@ __device__ int32_t big_tag(const SparseParams& p, int32_t nbig, int32_t ci) {
         MemberRec t = c.r[j];
         if (c.sp[j]) t.x = -1 - t.x;
         if (c.tu[j]) t.y |= (int32_t)0x80000000;  // touched: clear its marks in sub-phase 2
-        p.tmp[bs + ci0 + 32 * j + lane] = t;
+        p.tmp[(int64_t)ci * (32 * K) + 32 * j + lane] = t;  // chunk-major: see big_split
     }
     unsigned bal[K], kb[K];
     int32_t nsplit, nkeep, wmin;
@@ -289,7 +289,10 @@ __device__ void big_split(const SparseParams& p, int cur, int64_t round, int32_t
     for (int j = 0; j < K; ++j) {
         const int32_t i = ci0 + 32 * j + lane;
         c.valid[j] = i < bz;
-        MemberRec t = c.valid[j] ? p.tmp[bs + i] : make_int4(0, 0, 0, 0);
+        // tmp is chunk-major (chunk ci at ci * 32K), so every heavy round
+        // reuses the same few MB at the head of the array: its lines stay
+        // in L2 from round to round instead of being written back to HBM
+        MemberRec t = c.valid[j] ? p.tmp[(int64_t)ci * (32 * K) + 32 * j + lane] : make_int4(0, 0, 0, 0);
         c.sp[j] = c.valid[j] && t.x < 0;
         if (c.sp[j]) t.x = -1 - t.x;
         c.tu[j] = c.valid[j] && t.y < 0;
