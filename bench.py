@@ -456,6 +456,10 @@ def run_b200(args):
     achieved = bytes_alg / (t_alg / 1e3) / 1e9
     launches = sum(s.kernel_launches for s in sts)
     h2d = int(4 * m * (3 if inst.kind == "bcrp" else 2) + (4 * n if inst.kind == "rcpp" else 0))
+    # bytes that cross PCIe: the library narrows the actions of a large
+    # labelled system to 1 byte on the host first (capi.cu, pipelined path)
+    narrowed = inst.kind == "bcrp" and inst.num_actions <= 256 and m >= (1 << 22)
+    pcie = h2d - 3 * m if narrowed else h2d
     d2h = int(4 * n + 4 * R)
 
     result = None
@@ -482,7 +486,7 @@ def run_b200(args):
             "per_round_floor_us": floors,
             "rounds_retired": sts[0].rounds_retired,
             "e2e": {"value": e2e, "unit": UNIT, "ms_per_step": ms_e2e / args.steps,
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "pcie_h2d_bytes_per_step": pcie,
                     "path": "C ABI bisim_bcrp_ex/bisim_rcpp_ex, pinned host arrays, CUDA events"},
             "e2e_api": {"value": job_throughput(n + m, args.steps, world, ms_api), "unit": UNIT,
                         "ms_per_step": ms_api / args.steps, "h2d_bytes_per_step": h2d,
