@@ -198,7 +198,7 @@ struct SparseParams {
     int32_t* big_base4;
     int2* big_info;       // leader slot base / slot count of each big_list entry
     int2* big_info4;      // same for big_list4
-    int4* tmp;            // per member position: the record, x = -1-state if split
+    int4* tmp;            // two-pass records, chunk-major (chunk ci at ci * 32 kWide): x = -1-state if split
     SplitRec* srec;       // per label: arrival word and new-leader minimum (kernels_big.cuh)
     int32_t* scnt;        // per label: two-pass split count (its own line: the pass-1 reductions
                           //   of a block's chunks would otherwise queue behind its minimum's)
