@@ -135,3 +135,23 @@ def test_gpu_c5_other_ranks_lifted_truth(seed):
     block, st, _ = _run_gpu(inst)
     assert np.array_equal(block, inst.truth)
     assert st.final_block_count == len(np.unique(inst.truth))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("config", ["c5", "c4l", "c2"])
+@pytest.mark.parametrize("flags", ["FLAG_TWO_PASS|FLAG_NO_SOLO|FLAG_BATCH_WALK",
+                                   "FLAG_WIDE_LAYOUT|FLAG_NO_SKIP|FLAG_CTA_MAJOR"])
+def test_gpu_full_size_forced_layouts(config, flags):
+    """Every round of a full-size configuration through the heavy-round code
+    paths (two-pass split, batch registration wave, 128-member chunks, no
+    solo stretches / no bulk retirement): RunStats and block digest still
+    equal the oracle's run to completion."""
+    import bench
+    from paper_2105_11788_b200 import _native as N
+    f = 0
+    for part in flags.split("|"):
+        f |= getattr(N, part)
+    rec = _fixture(config)
+    inst, _ = bench.make_instance(config, 0)
+    block, st, ns = _run_gpu(inst, flags=f)
+    _check(rec, block, st, ns, f"{config} {flags}")
