@@ -476,6 +476,10 @@ __global__ void __launch_bounds__(kSparseThreads, kSparsePerSm) k_refine_sparse(
             // below needs it
             __syncthreads();
             if (threadIdx.x == 0) {
+                if (s_ctr_heavy) {  // the CTA registered a block of > 1 member
+                    red_or(&ctl->brec[cur][2], kRecFlag);
+                    s_ctr_heavy = 0;
+                }
                 unsigned* rec = ctl->arec[cur];
                 const unsigned target = ((cur ? genA1 : genA0) + 1u) * gridDim.x;
                 asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(rec) : "memory");

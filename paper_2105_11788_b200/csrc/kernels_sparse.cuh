@@ -471,10 +471,11 @@ __device__ __forceinline__ void register_blocks_warp(const SparseParams& p, int 
         nb = bi.nb;
     }
     const unsigned heavy = __ballot_sync(kFull, reg && r.y > 1);
-    if (heavy && lane == __ffs(heavy) - 1) {
-        if (solo) s_ctr_heavy = 1;
-        else red_or(&ctl->brec[cur][2], kRecFlag);
-    }
+    // the round's "touched a block of > 1 member" flag: per CTA in shared
+    // memory, one red per CTA at the mid barrier (a red per registering warp
+    // on the end-of-round record word queued thousands deep in c2's rounds,
+    // and each CTA's arrival release waited for its own)
+    if (heavy && lane == __ffs(heavy) - 1) s_ctr_heavy = 1;
     const unsigned small = __ballot_sync(kFull, reg && r.y <= 32);
     if (small) {
         const int ld = __ffs(small) - 1;
