@@ -457,6 +457,9 @@ __device__ int32_t big_onepass_cta(const SparseParams& p, int cur, int64_t round
                         (void)w3;
                         v = ((unsigned long long)w1 << 32) | w0;
                         mw = (int32_t)w2;
+#if BISIM_POLL_NS > 0
+                        if ((int32_t)(v >> kArrShift) < nch_b) __nanosleep(BISIM_POLL_NS);
+#endif
                     } while ((int32_t)(v >> kArrShift) < nch_b);
                     ns = (int32_t)((v >> kCntBits) & kCntMask);
                     w = ns ? mw : kBig;

@@ -491,6 +491,9 @@ __global__ void __launch_bounds__(kSparseThreads, kSparsePerSm) k_refine_sparse(
                         : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
                         : "l"(rec)
                         : "memory");
+#if BISIM_POLL_NS > 0
+                    if ((int)(w0 - target) < 0) __nanosleep(BISIM_POLL_NS);
+#endif
                 } while ((int)(w0 - target) < 0);
                 s_snap[0] = (int32_t)w1;
                 s_snap[1] = (long long)(((unsigned long long)w3 << 32) | w2);
@@ -634,6 +637,9 @@ __global__ void __launch_bounds__(kSparseThreads, kSparsePerSm) k_refine_sparse(
                         : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
                         : "l"(rec)
                         : "memory");
+#if BISIM_POLL_NS > 0
+                    if ((int)(w0 - target) < 0) __nanosleep(BISIM_POLL_NS);
+#endif
                 } while ((int)(w0 - target) < 0);
                 const int32_t c_next = (int32_t)(w1 >> 1);  // ~0u -> kBig
                 s_snap[3] = c_next;
