@@ -378,3 +378,28 @@ def _pipelined_oracle(inst):
     if inst.name not in _PIPE_ORACLE:
         _PIPE_ORACLE[inst.name] = oracle.bcrp_fast(inst.n, inst.src, inst.act, inst.dst, inst.num_actions)
     return _PIPE_ORACLE[inst.name]
+
+
+@pytest.mark.parametrize("n,m,A,null_src", [(0, 0, 1, False), (1 << 30, 0, 1, False), (10, 1 << 31, 1, True),
+                                            (10, 5, 1, True), (10, 0, -1, False), (-3, 0, 1, False)])
+def test_c_abi_size_limits(n, m, A, null_src):
+    """The C ABI's documented limits (include/bisim.h: 1 <= n < 2^30,
+    0 <= m < 2^31 - 1, |Act| >= 0, non-null arrays when m > 0) are checked
+    before anything is allocated or copied: BISIM_BAD_INPUT with a message,
+    and the device stays usable."""
+    import ctypes
+    lib = N.lib()
+    src = np.zeros(max(min(m, 8), 1), np.int32)
+    block = np.zeros(16, np.int32)
+    splits = np.zeros(16, np.int32)
+    st = N.Stats()
+    opt = N.Options()
+    p_src = None if null_src else N.ptr(src)
+    rc = lib.bisim_bcrp_ex(n, m, A, p_src, p_src, p_src, N.DEFAULT_GUARD, N.ptr(block), N.ptr(splits), 16,
+                           ctypes.byref(st), ctypes.byref(opt))
+    assert rc == N.BISIM_BAD_INPUT, rc
+    assert lib.bisim_last_error()
+    rec = G.cases()["pre_fig2"]
+    nn, s, a, d, AA = G.arrays(rec)
+    blk, _, _ = bcrp_arrays(nn, s, a, d, AA)
+    assert list(blk) == rec["bcrp"]["block"]
